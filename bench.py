@@ -1,0 +1,479 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native batched signature transform (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A "step" is one pass of the hot path (sigk_signature_f32 through the C ABI)
+over one batch. Default workload = BASELINE.json configs[1]: B=128 paths,
+L=1000, d=5, depth N=4, fp32, synthetic Brownian paths (X0 = 0, increments
+N(0, 1/(L-1)), Philox keyed by (seed, row, t, c)). Under torchrun each rank
+processes its own B=128 rows (weak scaling, no data-path collective); timings
+are the max over ranks.
+
+value  : device-resident inputs (a pool of input batches larger than the
+         126 MB L2, rotated every step), K steps captured in CUDA graphs and
+         replayed on one stream, CUDA events around the whole region.
+e2e    : the same call with HOST (pinned) buffers: H2D of the step's paths,
+         kernels, D2H of the step's signatures, every step.
+roofline: the fold kernel (the dominant kernel) timed with CUDA events on its
+         launch stream inside the timed graphs; achieved = credited FP32 flops
+         per launch / mean fold duration, against an FFMA-pipe peak measured
+         on this GPU by a register-resident microbenchmark.
+cpu_baseline: the reference's own sequential_forward<double> compiled from its
+         sources (oracle/_ref; else the C port), all host threads, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": (32, 100, 2, 4),
+    "c2": (128, 1000, 5, 4),
+    "c3": (128, 10000, 5, 4),
+    "c4": (64, 500, 10, 5),
+    "c5": (8192, 1000, 8, 4),
+}
+L2_BYTES = 126 * 1024 * 1024
+NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def baseline_metric():
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        return json.load(f)["metric"]
+
+
+def work_per_path(L, d, N):
+    """credited flops F = 2 W (L-1), W = Σ_k (N-k+1) d^k; bytes = 4 (L d + D)."""
+    W = sum((N - k + 1) * d ** k for k in range(1, N + 1))
+    D = sum(d ** n for n in range(1, N + 1))
+    return 2.0 * W * (L - 1), 4.0 * (L * d + D), W, D
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """NVML SM clock + clocks-event reasons sampled every 10 ms while running."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock"}
+
+    def __init__(self, index):
+        self.index, self.samples, self.reasons, self._stop = index, [], 0, threading.Event()
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        s = sorted(self.samples)
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- CPU arms
+def cpu_reference_run(X64, N, threads):
+    """One pass of the reference CPU path; returns (seconds, kind)."""
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    if O.ref() is not None:
+        O.ref_forward(X64, N, threads=threads)
+        kind = "reference"
+    else:
+        O.signature(X64, N, threads=threads)
+        kind = "port"
+    return time.perf_counter() - t0, kind
+
+
+def cpu_baseline(X32, N, budget_s=6.0):
+    """Reference sequential_forward<double> (what signature_sequential runs) on the
+    same fp32 inputs promoted to double, all host threads, repeated ~budget_s."""
+    import numpy as np
+
+    threads = os.cpu_count() or 1
+    X64 = X32.astype(np.float64)
+    B = X64.shape[0]
+    # bound the sample: at most ~1 s per pass
+    t1, kind = cpu_reference_run(X64[: max(1, min(B, threads))], N, threads)
+    per_row = t1 / max(1, min(B, threads)) * threads
+    rows = int(min(B, max(threads, 1.0 / max(per_row / threads, 1e-9))))
+    rows = max(1, min(B, rows))
+    Xs = X64[:rows]
+    best, total, reps = float("inf"), 0.0, 0
+    while total < budget_s and reps < 1000:
+        dt, kind = cpu_reference_run(Xs, N, threads)
+        best, total, reps = min(best, dt), total + dt, reps + 1
+    return {"value": rows / best, "unit": "paths/s", "cores": threads, "kind": kind,
+            "sample": f"{rows} of {B} rows, best of {reps} passes ({total:.1f} s wall)",
+            "seconds_best": best}
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2501_08455_b200 as sk
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    B, L, d, N = CONFIGS[args.config]
+    flops_path, bytes_path, W, D = work_per_path(L, d, N)
+    stream = torch.cuda.Stream(device=dev)
+
+    # input pool larger than L2 (rotated every step), distinct rows per rank
+    in_bytes = B * L * d * 4
+    n_buf = 2 if in_bytes > L2_BYTES else min(256, math.ceil(2 * L2_BYTES / in_bytes))
+    pool = torch.empty((n_buf, B, L, d), dtype=torch.float32, device=dev)
+    with torch.cuda.stream(stream):
+        for i in range(n_buf):
+            sk.brownian(pool[i], seed=42 + i, row0=rank * B)
+    out = torch.empty((B, D), dtype=torch.float32, device=dev)
+    stream.synchronize()
+
+    st = sk.KernelStats()
+    with torch.cuda.stream(stream):
+        sk.signature(pool[0], N, stats=st, out=out)
+    stream.synchronize()
+
+    # FFMA-pipe peak on this GPU (roofline denominator)
+    import ctypes as C
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.empty(sms * 8 * 256, dtype=torch.float32, device=dev)
+    fl = C.c_double(0)
+    peak = 0.0
+    with torch.cuda.stream(stream):
+        for rep in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sk.lib().sigk_bench_ffma(sink.data_ptr(), sms * 8, 2000, C.byref(fl), C.c_void_p(stream.cuda_stream))
+            e1.record(stream)
+            e1.synchronize()
+            if rep:
+                peak = max(peak, fl.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+
+    # graphs: S distinct steps per graph, every 4th step's fold kernel bracketed by events
+    S = min(args.steps, n_buf, 64)
+    step_events = []
+
+    def capture(nsteps, with_events):
+        g = torch.cuda.CUDAGraph()
+        evs = {}
+        if with_events:  # create the CUDA events (torch creates them lazily on first record)
+            for j in range(0, nsteps, 4):
+                evs[j] = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                evs[j][0].record(stream)
+                evs[j][1].record(stream)
+            stream.synchronize()
+        with torch.cuda.graph(g, stream=stream):
+            for j in range(nsteps):
+                _step(sk, pool[j % n_buf], N, out, evs.get(j))
+        return g, list(evs.values())
+
+    # warm-up (eager + one graph replay)
+    with torch.cuda.stream(stream):
+        for j in range(args.warmup):
+            _step(sk, pool[j % n_buf], N, out, None)
+    stream.synchronize()
+    reps_full, rem = divmod(args.steps, S)
+    g_main, ev_main = capture(S, True)
+    g_rem = capture(rem, False)[0] if rem else None
+    for _ in range(max(1, args.warmup // S)):
+        g_main.replay()
+    torch.cuda.synchronize()
+
+    clk = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clk:
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+            for _ in range(reps_full):
+                g_main.replay()
+            if g_rem is not None:
+                g_rem.replay()
+            t1.record(stream)
+        t1.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    elapsed = max_over_ranks(t0.elapsed_time(t1) * 1e-3, world)
+    fold_ms = [a.elapsed_time(b) for a, b in ev_main]
+    fold_s = max_over_ranks(sum(fold_ms) / len(fold_ms) * 1e-3, world)
+
+    # single-launch (non-graph) latency of one step, for reference
+    with torch.cuda.stream(stream):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _step(sk, pool[0], N, out, None)
+        b.record(stream)
+    b.synchronize()
+    single_ms = a.elapsed_time(b)
+
+    # e2e through the C ABI with host (pinned) buffers
+    Xh = pool[0].cpu().pin_memory()
+    outh = torch.empty((B, D), dtype=torch.float32).pin_memory()
+    lib = sk.lib()
+    tun = sk._Tuning()
+    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    for _ in range(3):
+        sk._check(lib.sigk_signature_f32(Xh.data_ptr(), B, L, d, N, outh.data_ptr(), 0,
+                                         C.c_void_p(stream.cuda_stream), C.byref(tun), None))
+    barrier(world)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        sk._check(lib.sigk_signature_f32(Xh.data_ptr(), B, L, d, N, outh.data_ptr(), 0,
+                                         C.c_void_p(stream.cuda_stream), C.byref(tun), None))
+    e1.record(stream)
+    e1.synchronize()
+    wall = time.perf_counter() - w0
+    e2e_s = max_over_ranks(max(e0.elapsed_time(e1) * 1e-3, wall), world)
+
+    # parity spot check of this run's output (first rows) against the oracle
+    parity = None
+    if rank == 0:
+        from oracle import oracle as O
+
+        rows = min(B, 8)
+        ref = O.signature(Xh[:rows].numpy().astype(np.float64), N, threads=os.cpu_count() or 1)
+        got = outh[:rows].numpy().astype(np.float64)
+        off = O.level_offsets(d, N)
+        parity = max(float(np.abs(got[:, off[n]:off[n + 1]] - ref[:, off[n]:off[n + 1]]).max()
+                         / np.abs(ref[:, off[n]:off[n + 1]]).max()) for n in range(N))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(pool[0].cpu().numpy(), N)
+        cpu.pop("seconds_best", None)
+
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+    steps = args.steps
+    value = world * B * steps / elapsed
+    achieved = B * flops_path / fold_s / 1e12
+    traffic = _traffic(args.config)
+    peaks = load_peaks()
+    line = {
+        "metric": baseline_metric(),
+        "value": value,
+        "unit": "paths/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": args.warmup,
+        "ms_per_step": elapsed / steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic Brownian paths (Philox, X0=0, N(0,1/(L-1)) increments), generated on device",
+        "config": {
+            "workload": f"{args.config}: B={B} L={L} d={d} N={N} fp32 batched truncated signature per GPU"
+                        + (" (BASELINE.json configs[1], headline)" if args.config == "c2" else ""),
+            "batch_per_gpu": B, "global_batch": B * world, "seq_len": L, "dim": d, "depth": N, "sig_dim": D,
+            "parallelism": f"batch-sharded x{world}, no collective",
+            "l2": f"inputs rotate over {n_buf} device batches = {n_buf * in_bytes / 2**20:.0f} MiB (> 126 MB L2)",
+            "timing": f"{steps} steps = CUDA graph of {S} steps x {reps_full}"
+                      + (f" + {rem}" if rem else "") + "; CUDA events on the launch stream; max over ranks",
+            "chunks": st.chunks, "prefix_len": st.prefix_len, "threads_per_unit": st.threads_per_unit,
+            "fold_steps_per_unit": st.fold_steps, "merge_rounds": st.scan_passes,
+            "single_launch_ms": single_ms,
+            "parity_max_level_rel_err": parity,
+        },
+        "roofline": {
+            "bound": "fp32",
+            "kernel": "fold_kernel (FFMA-pipe bound; tensor cores deliberately unused, SURVEY.md §8d)",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None,
+            "peak_source": "measured: register-resident FFMA microbenchmark on this GPU (sigk_bench_ffma); "
+                           f"nominal {NOMINAL_FP32_TFLOPS:.2f}",
+            "credited_flops_per_launch": B * flops_path,
+            "fold_ms_mean": fold_s * 1e3,
+            "fold_share_of_step": fold_s / (elapsed / steps),
+            "step_frac_of_roof": (B * flops_path / (elapsed / steps)) / 1e12 / peak if peak else None,
+            "hbm": {"algorithmic_bytes_per_launch": B * bytes_path,
+                    "achieved_gbs": B * bytes_path / fold_s / 1e9,
+                    "peak_gbs": peaks.get("hbm_gbs"), "peak_source": "MEASURED_PEAKS.json"},
+            "traffic": traffic,
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * B * e2e_steps / e2e_s, "unit": "paths/s",
+                "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": B * D * 4, "steps": e2e_steps,
+                "api": "sigk_signature_f32 (C ABI), pinned host buffers, synchronous per step"},
+        "clocks": clk.summary(),
+        "gpu_launches": steps * max(1, st.launches),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _step(sk, X, N, out, ev):
+    import ctypes as C
+
+    import torch
+
+    tun = sk._Tuning()
+    if ev is not None:
+        tun.fold_event_start = C.c_void_p(ev[0].cuda_event)
+        tun.fold_event_stop = C.c_void_p(ev[1].cuda_event)
+    B, L, d = X.shape
+    s = torch.cuda.current_stream()
+    sk._check(sk.lib().sigk_signature_f32(X.data_ptr(), B, L, d, N, out.data_ptr(),
+                                          sk.SIGK_X_ON_DEVICE | sk.SIGK_OUT_ON_DEVICE,
+                                          C.c_void_p(s.cuda_stream), C.byref(tun), None))
+
+
+def _traffic(config):
+    """dram bytes per fold launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(config)
+    except (OSError, ValueError):
+        return None
+
+
+def run_reference(args):
+    """The reference's own CPU implementation (oracle/_ref: the reference compiled
+    from its sources; else the C port), all host threads, rank 0 only."""
+    import numpy as np
+
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    B, L, d, N = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(42)
+    X = np.zeros((B, L, d), np.float64)
+    X[:, 1:] = np.cumsum(rng.standard_normal((B, L - 1, d)) / math.sqrt(L - 1), axis=1)
+    X = X.astype(np.float32).astype(np.float64)  # same fp32-representable inputs as the GPU arm
+    # bounded sample per step: enough rows for ~1 s of work on all threads
+    t1, kind = cpu_reference_run(X[:threads], N, threads)
+    rows = int(max(1, min(B, threads * max(1.0, 1.0 / max(t1, 1e-6)))))
+    Xs = X[:rows]
+    for _ in range(args.warmup):
+        cpu_reference_run(Xs, N, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, kind = cpu_reference_run(Xs, N, threads)
+    dt = time.perf_counter() - t0
+    value = rows * args.steps / dt
+    line = {
+        "metric": baseline_metric(), "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic Brownian paths (numpy, seed 42)",
+        "impl": "reference",
+        "config": {"workload": f"{args.config}: B={B} L={L} d={d} N={N}", "batch_per_step": rows,
+                   "seq_len": L, "dim": d, "depth": N},
+        "cpu_baseline": {"value": value, "unit": "paths/s", "cores": threads, "kind": kind,
+                         "sample": f"{rows} of {B} rows per step, sigkit_ref::detail::sequential_forward<double>"},
+        "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        args.steps = args.steps or 5
+        args.warmup = 1 if args.warmup is None else args.warmup
+        run_reference(args)
+        return
+    default_steps = {"c1": 20000, "c2": 20000, "c3": 2000, "c4": 500, "c5": 100}[args.config]
+    args.steps = args.steps or default_steps
+    args.warmup = max(3, args.warmup if args.warmup is not None else 50)
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

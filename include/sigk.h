@@ -1,0 +1,127 @@
+/*
+ * sigk.h — C ABI of the B200-native batched truncated path-signature transform.
+ *
+ * This is the drop-in boundary. Every entry point replaces a
+ * reference interface, cited below by file:line in /root/reference/proj:
+ *
+ *   sigk_sig_dim          ← sigkit::sig_dim            include/sigkit/tensor_algebra.hpp:35, src/tensor_algebra.cpp:10-20
+ *   sigk_level_offsets    ← sigkit::level_offsets      include/sigkit/tensor_algebra.hpp:42, src/tensor_algebra.cpp:33-41
+ *   sigk_signature_f64    ← sigkit::signature / signature_sequential / signature_parallel
+ *                           include/sigkit/kernels.hpp:100-124, src/kernels.cpp:106-148,200-206
+ *                           (the double-precision public API; same layout and results)
+ *   sigk_signature_f32    ← detail::sequential_forward<float>
+ *                           include/sigkit/detail/sig_core.hpp:120-147 (the raw-pointer core the
+ *                           reference bench instantiates for float, src/bench.cpp:29-56)
+ *   sigk_signature_sharded_f32/_f64
+ *                         ← signature() over a batch split across GPUs (rows are independent,
+ *                           SPEC.md:220-221; tests/test_kernels.cpp:252-263)
+ *   sigk_last_error       ← the what() string of the reference exceptions (errors.hpp:9-36)
+ *
+ * Layouts (identical to the reference, sig_core.hpp:7-10):
+ *   paths      (B, L, d)  row-major, element ((b*L + t)*d + c)
+ *   signatures (B, D)     D = sum_{n=1..N} d^n; level n at offset sum_{m<n} d^m,
+ *                         row-major inside a level, first index = earliest increment.
+ *
+ * Conventions: plain pointers and sizes, no ownership transfer (the caller
+ * owns every buffer; the library never frees caller memory). L == 1 yields
+ * all-zero rows (the identity, sig_core.hpp:201-206). Results are
+ * deterministic: the fold/merge order depends only on (B, L, d, N) and the
+ * chosen chunking, never on the launch or on timing.
+ *
+ * Return codes: SIGK_OK, SIGK_EDOMAIN (the reference's DomainError checks,
+ * kernels.cpp:13-26 / tensor_algebra.cpp:11-12), SIGK_ERESOURCE (device
+ * allocation failure; the reference's ResourceError), SIGK_EDEVICE (a CUDA
+ * error, text in sigk_last_error). There is no CPU fallback: with no usable
+ * GPU every compute entry point returns SIGK_EDEVICE.
+ */
+#ifndef SIGK_H
+#define SIGK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SIGK_OK 0
+#define SIGK_EDOMAIN 1
+#define SIGK_ERESOURCE 2
+#define SIGK_EDEVICE 3
+
+/* flags for sigk_signature_*: where the buffers live. Without a flag the
+ * buffer is host memory and the call is synchronous (H2D, kernels, D2H). With
+ * both flags set the call is asynchronous on `stream` (cudaStream_t, NULL =
+ * the legacy default stream) and touches no host memory. */
+#define SIGK_X_ON_DEVICE 1u
+#define SIGK_OUT_ON_DEVICE 2u
+
+/* Structural counters (the reference KernelStats, kernels.hpp:86-91, plus
+ * the GPU decomposition). fold_steps = increments folded by each (path,
+ * chunk) unit = ceil((L-1)/chunks); scan_passes = depth of the Chen
+ * merge tree = ceil(log2(chunks)). */
+typedef struct sigk_stats {
+    int64_t fold_steps;
+    int64_t scan_passes;
+    int32_t chunks;       /* K: chunks per path along the sequence axis */
+    int32_t prefix_len;   /* Q: leading indices owned per thread (-1: generic kernel) */
+    int32_t threads_per_unit; /* d^Q */
+    int32_t launches;     /* kernels launched by the call */
+} sigk_stats;
+
+/* Optional tuning overrides (NULL or zero fields = automatic). */
+typedef struct sigk_tuning {
+    int32_t chunks;       /* force K >= 1 */
+    int32_t force_generic;/* 1: route to the shape-generic kernel */
+    int64_t plan_rows;    /* plan K as if the batch had this many rows (0: B).
+                             Results are bitwise independent of the batch
+                             composition whenever K is the same, so callers
+                             that split a batch (sigk_signature_sharded_*)
+                             pass the global row count here. */
+    void* fold_event_start; /* optional cudaEvent_t recorded on the stream just
+                               before the fold kernel (instrumentation) */
+    void* fold_event_stop;  /* ... and just after it */
+    int32_t reserved[4];
+} sigk_tuning;
+
+int sigk_sig_dim(int d, int N, size_t* D);
+int sigk_level_offsets(int d, int N, size_t* offsets /* N+1 entries */);
+
+int sigk_signature_f32(const float* X, size_t B, size_t L, int d, int N, float* out, unsigned flags,
+                       void* stream, const sigk_tuning* tuning, sigk_stats* stats);
+int sigk_signature_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags,
+                       void* stream, const sigk_tuning* tuning, sigk_stats* stats);
+
+/* Host buffers in and out; rows [g*ceil(B/G), ...) run on device g, one host
+ * thread per device, each shard copied in, folded and copied back into its
+ * disjoint slice of `out`. num_gpus <= 0 means all visible devices. */
+int sigk_signature_sharded_f32(const float* X, size_t B, size_t L, int d, int N, float* out, int num_gpus,
+                               sigk_stats* stats);
+int sigk_signature_sharded_f64(const double* X, size_t B, size_t L, int d, int N, double* out, int num_gpus,
+                               sigk_stats* stats);
+
+/* Synthetic benchmark input on the device: Brownian paths,
+ * X[b,0,:] = 0, increments N(0, 1/(L-1)) from Philox4x32-10 keyed by
+ * (seed, row0 + b, t, c) — identical rows for any sharding. */
+int sigk_brownian_f32(float* X_dev, size_t B, size_t L, int d, uint64_t seed, size_t row0, void* stream);
+int sigk_brownian_f64(double* X_dev, size_t B, size_t L, int d, uint64_t seed, size_t row0, void* stream);
+
+/* 1 when a register-sliced fast variant exists for (d, N) in this precision
+ * (0: the shape-generic kernel is used). *Q receives the prefix length. */
+int sigk_has_fast_variant(int d, int N, int is_f64, int* Q);
+
+/* FP32 FFMA-pipe peak microbenchmark (roofline denominator): launches
+ * `blocks` x 256 threads, each running iters*128 independent-chain FFMAs;
+ * *flops = 2 x FFMAs. Time it with events on `stream`. */
+int sigk_bench_ffma(float* sink, int blocks, int iters, double* flops, void* stream);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* sigk_last_error(void);
+
+/* ABI version: major*10000 + minor*100 + patch. */
+int sigk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIGK_H */

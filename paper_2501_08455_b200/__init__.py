@@ -1,0 +1,282 @@
+"""B200-native batched truncated path-signature transform (arXiv 2501.08455).
+
+Python host-side mirror of the reference public API
+(/root/reference/proj/include/sigkit/kernels.hpp:12-124,
+tensor_algebra.hpp:35-42): ``signature``, ``signature_sequential``,
+``signature_parallel``, ``select_kernel``, ``sig_dim``, ``level_offsets``,
+``KernelKind``, ``ExecutionCaps``, ``KernelStats`` and the error classes, over
+the C ABI of ``libsigk.so`` (include/sigk.h). Every compute call runs the
+sm_100a kernels; if the library is missing or no GPU is usable the call
+raises — there is no CPU fallback.
+
+Inputs may be numpy arrays (host buffers: the library stages them through
+the device and returns numpy) or CUDA torch tensors (device buffers: the call
+is asynchronous on the current torch stream and returns a CUDA tensor).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsigk.so")
+
+SIGK_OK, SIGK_EDOMAIN, SIGK_ERESOURCE, SIGK_EDEVICE = 0, 1, 2, 3
+SIGK_X_ON_DEVICE, SIGK_OUT_ON_DEVICE = 1, 2
+
+
+class DomainError(ValueError):
+    """Bad shapes/arguments (reference errors.hpp:9-12)."""
+
+
+class ResourceError(RuntimeError):
+    """Capacity failure (reference errors.hpp:16-19)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure on the device path."""
+
+
+class _Stats(C.Structure):
+    _fields_ = [("fold_steps", C.c_int64), ("scan_passes", C.c_int64), ("chunks", C.c_int32),
+                ("prefix_len", C.c_int32), ("threads_per_unit", C.c_int32), ("launches", C.c_int32)]
+
+
+class _Tuning(C.Structure):
+    _fields_ = [("chunks", C.c_int32), ("force_generic", C.c_int32), ("plan_rows", C.c_int64),
+                ("fold_event_start", C.c_void_p), ("fold_event_stop", C.c_void_p), ("reserved", C.c_int32 * 4)]
+
+
+@dataclass
+class KernelStats:
+    """Reference KernelStats (kernels.hpp:86-91) plus the GPU decomposition."""
+    fold_steps: int = 0
+    scan_passes: int = 0
+    chunks: int = 0
+    prefix_len: int = 0
+    threads_per_unit: int = 0
+    launches: int = 0
+
+
+class KernelKind(enum.Enum):
+    Sequential = "sequential"
+    Parallel = "parallel"
+    Auto = "auto"
+
+
+def kernel_name(kind: KernelKind) -> str:
+    return kind.value
+
+
+def kernel_from_name(name: str) -> KernelKind:
+    for k in KernelKind:
+        if k.value == name:
+            return k
+    raise DomainError(f"unknown kernel '{name}', expected sequential, parallel or auto")
+
+
+@dataclass
+class ExecutionCaps:
+    """Reference kernels.hpp:76-84; kept for source compatibility."""
+    accelerated: bool = True
+    parallel_min_len: int = 64
+
+    @staticmethod
+    def detect() -> "ExecutionCaps":
+        env = os.environ.get("SIGKIT_ACCELERATED")
+        return ExecutionCaps(accelerated=env is None or env != "0")
+
+
+def select_kernel(hint: KernelKind, caps: ExecutionCaps, seq_len: int) -> KernelKind:
+    if hint != KernelKind.Auto:
+        return hint
+    return KernelKind.Parallel if (caps.accelerated and seq_len >= caps.parallel_min_len) else KernelKind.Sequential
+
+
+_lib = None
+
+
+def lib():
+    """The loaded libsigk.so; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        sz, vp = C.c_size_t, C.c_void_p
+        L.sigk_sig_dim.argtypes = [C.c_int, C.c_int, C.POINTER(sz)]
+        L.sigk_level_offsets.argtypes = [C.c_int, C.c_int, C.POINTER(sz)]
+        for n in ("sigk_signature_f32", "sigk_signature_f64"):
+            getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, C.c_uint, vp, C.POINTER(_Tuning),
+                                      C.POINTER(_Stats)]
+        for n in ("sigk_signature_sharded_f32", "sigk_signature_sharded_f64"):
+            getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, C.c_int, C.POINTER(_Stats)]
+        for n in ("sigk_brownian_f32", "sigk_brownian_f64"):
+            getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_uint64, sz, vp]
+        L.sigk_has_fast_variant.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        L.sigk_last_error.restype = C.c_char_p
+        L.sigk_bench_ffma.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double), vp]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc == SIGK_OK:
+        return
+    msg = lib().sigk_last_error().decode()
+    if rc == SIGK_EDOMAIN:
+        raise DomainError(msg)
+    if rc == SIGK_ERESOURCE:
+        raise ResourceError(msg)
+    raise DeviceError(msg)
+
+
+def sig_dim(dim: int, depth: int) -> int:
+    """D = Σ_{n=1..N} d^n (reference tensor_algebra.cpp:10-20)."""
+    D = C.c_size_t(0)
+    _check(lib().sigk_sig_dim(dim, depth, C.byref(D)))
+    return D.value
+
+
+def level_offsets(dim: int, depth: int) -> list[int]:
+    """offsets[n-1] = start of degree n, offsets[N] = D (tensor_algebra.cpp:33-41)."""
+    if depth < 1:
+        _check(lib().sigk_sig_dim(dim, depth, None))
+    off = (C.c_size_t * (depth + 1))()
+    _check(lib().sigk_level_offsets(dim, depth, off))
+    return list(off)
+
+
+def level_sizes(dim: int, depth: int) -> list[int]:
+    off = level_offsets(dim, depth)
+    return [off[i + 1] - off[i] for i in range(depth)]
+
+
+def has_fast_variant(dim: int, depth: int, f64: bool = False) -> tuple[bool, int]:
+    q = C.c_int(0)
+    ok = lib().sigk_has_fast_variant(dim, depth, int(f64), C.byref(q))
+    return bool(ok), q.value
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _validate_shape(shape, depth):
+    if len(shape) != 3:
+        raise DomainError(f"paths must have shape (B, L, d), got {tuple(shape)}")
+    B, L, d = (int(s) for s in shape)
+    if B < 1 or L < 1 or d < 1:
+        raise DomainError("paths: batch, len and dim must all be >= 1")
+    if depth < 1:
+        raise DomainError(f"depth must be >= 1, got {depth}")
+    return B, L, d
+
+
+def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_generic: bool = False,
+         out=None, plan_rows: int = 0):
+    st = _Stats()
+    tun = _Tuning(chunks=chunks, force_generic=int(force_generic), plan_rows=plan_rows)
+    if _is_torch(paths):
+        import torch
+
+        if not paths.is_cuda:
+            raise DomainError("torch input must be a CUDA tensor (use numpy for host buffers)")
+        B, L, d = _validate_shape(paths.shape, depth)
+        if paths.dtype not in (torch.float32, torch.float64):
+            raise DomainError(f"unsupported dtype {paths.dtype}")
+        X = paths.contiguous()
+        D = sig_dim(d, depth)
+        if out is None:
+            out = torch.empty((B, D), dtype=X.dtype, device=X.device)
+        fn = lib().sigk_signature_f32 if X.dtype == torch.float32 else lib().sigk_signature_f64
+        with torch.cuda.device(X.device):
+            s = torch.cuda.current_stream(X.device).cuda_stream
+            _check(fn(X.data_ptr(), B, L, d, depth, out.data_ptr(), SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE,
+                      s, C.byref(tun), C.byref(st)))
+    else:
+        X = np.asarray(paths)
+        B, L, d = _validate_shape(X.shape, depth)
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        X = np.ascontiguousarray(X)
+        D = sig_dim(d, depth)
+        out = np.empty((B, D), dtype=X.dtype) if out is None else out
+        fn = lib().sigk_signature_f32 if X.dtype == np.float32 else lib().sigk_signature_f64
+        _check(fn(X.ctypes.data, B, L, d, depth, out.ctypes.data, 0, None, C.byref(tun), C.byref(st)))
+    if stats is not None:
+        for f, _ in _Stats._fields_:
+            setattr(stats, f, getattr(st, f))
+    return out
+
+
+def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
+              stats: KernelStats | None = None, *, chunks: int = 0, out=None, plan_rows: int = 0):
+    """Reference ``sigkit::signature`` (kernels.cpp:200-206): (B, L, d) -> (B, D).
+
+    ``kernel``/``caps`` are accepted for source compatibility; every kind runs
+    the same GPU kernels. ``chunks`` forces the sequence split (0 = planned);
+    ``plan_rows`` plans the split as if the batch had that many rows (results
+    are bitwise independent of batch composition at equal chunking).
+    """
+    select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
+    return _run(paths, depth, stats, chunks=chunks, out=out, plan_rows=plan_rows)
+
+
+def signature_sequential(paths, depth: int, stats: KernelStats | None = None, **kw):
+    """Reference ``signature_sequential`` (kernels.cpp:106-122)."""
+    return _run(paths, depth, stats, **kw)
+
+
+def signature_parallel(paths, depth: int, stats: KernelStats | None = None, memory_cap: int = 1 << 31, **kw):
+    """Reference ``signature_parallel`` (kernels.cpp:124-148), including its
+    ResourceError refusal above ``memory_cap`` scalars (sig_core.hpp:161-173)."""
+    B, L, d = _validate_shape(np.shape(paths), depth)
+    if float(B) * L * float(d) ** depth > memory_cap:
+        raise ResourceError(f"parallel kernel: intermediate storage of ~{float(B) * L * float(d) ** depth:g} "
+                            f"scalars exceeds cap {memory_cap}; use the sequential kernel for this shape")
+    return _run(paths, depth, stats, **kw)
+
+
+def signature_generic(paths, depth: int, stats: KernelStats | None = None):
+    """Force the shape-generic GPU kernel (cross-check of the sliced variants)."""
+    return _run(paths, depth, stats, force_generic=True)
+
+
+def signature_sharded(paths: np.ndarray, depth: int, num_gpus: int = 0, stats: KernelStats | None = None):
+    """Host buffers in/out, batch rows sharded across ``num_gpus`` devices."""
+    X = np.ascontiguousarray(paths)
+    B, L, d = _validate_shape(X.shape, depth)
+    if X.dtype not in (np.float32, np.float64):
+        X = X.astype(np.float64)
+    out = np.empty((B, sig_dim(d, depth)), dtype=X.dtype)
+    st = _Stats()
+    fn = lib().sigk_signature_sharded_f32 if X.dtype == np.float32 else lib().sigk_signature_sharded_f64
+    _check(fn(X.ctypes.data, B, L, d, depth, out.ctypes.data, num_gpus, C.byref(st)))
+    if stats is not None:
+        for f, _ in _Stats._fields_:
+            setattr(stats, f, getattr(st, f))
+    return out
+
+
+def brownian(out, seed: int = 42, row0: int = 0):
+    """Fill a CUDA tensor (B, L, d) with synthetic Brownian paths (sigk_brownian_*)."""
+    import torch
+
+    B, L, d = out.shape
+    fn = lib().sigk_brownian_f32 if out.dtype == torch.float32 else lib().sigk_brownian_f64
+    with torch.cuda.device(out.device):
+        _check(fn(out.data_ptr(), B, L, d, seed, row0, torch.cuda.current_stream(out.device).cuda_stream))
+    return out
+
+
+__all__ = [
+    "DomainError", "ResourceError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
+    "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
+    "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
+    "has_fast_variant", "lib",
+]

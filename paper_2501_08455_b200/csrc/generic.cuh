@@ -1,0 +1,109 @@
+// Shape-generic fold for (d, N) pairs without a register-sliced instantiation.
+//
+// Same recurrence as fold.cuh (reference sig_core.hpp:92-114), evaluated
+// element-parallel instead of slice-parallel: one CTA per path keeps the flat
+// state row in global memory (L2-resident), and for each step updates the
+// levels in descending order, one CTA barrier per level:
+//     T_n[I] += Σ_{j=1}^{n} T_{n-j}[I / d^j] · Π_{last j digits c of I} δ[c] / j!
+// with T_0 = 1. Slow (O(N·D) work and N barriers per step) but correct for
+// any shape; the dispatcher only routes here when no fast variant exists.
+#pragma once
+
+#include "sigk_common.cuh"
+
+namespace sigk {
+
+constexpr int kGenericMaxDepth = 16;
+
+template <typename Real>
+__global__ void __launch_bounds__(256) generic_fold_kernel(const Real* __restrict__ X, int64_t L, int d, int N,
+                                                           int64_t D, Real* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* dl = reinterpret_cast<Real*>(smem_raw);  // [d]
+    __shared__ int64_t off[kGenericMaxDepth + 1];
+    __shared__ Real invfact[kGenericMaxDepth + 1];
+    const int64_t b = blockIdx.x;
+    Real* S = out + b * D;
+    if (threadIdx.x == 0) {
+        off[0] = 0;
+        int64_t p = 1;
+        Real f = 1;
+        invfact[0] = 1;
+        for (int n = 1; n <= N; ++n) {
+            p *= d;
+            off[n] = off[n - 1] + p;
+            f *= Real(n);
+            invfact[n] = Real(1) / f;
+        }
+    }
+    for (int64_t i = threadIdx.x; i < D; i += blockDim.x) S[i] = Real(0);
+    const Real* row = X + b * L * d;
+    for (int64_t t = 0; t + 1 < L; ++t) {
+        __syncthreads();
+        for (int c = threadIdx.x; c < d; c += blockDim.x) dl[c] = row[(t + 1) * d + c] - row[t * d + c];
+        __syncthreads();
+        for (int n = N; n >= 1; --n) {
+            const int64_t lsz = off[n] - off[n - 1];
+            for (int64_t I = threadIdx.x; I < lsz; I += blockDim.x) {
+                Real acc = S[off[n - 1] + I];
+                Real e = 1;
+                int64_t rem = I;
+                for (int j = 1; j <= n; ++j) {
+                    e *= dl[rem % d];
+                    rem /= d;
+                    const Real lower = (j < n) ? S[off[n - j - 1] + rem] : Real(1);
+                    acc = fma(lower, e * invfact[j], acc);
+                }
+                S[off[n - 1] + I] = acc;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Synthetic Brownian paths for the benchmark: X[b,0,:] = 0,
+// X[b,t,c] = X[b,t-1,c] + σ·Z, σ = 1/sqrt(L-1), Z ~ N(0,1) from a
+// counter-based Philox4x32-10 keyed by (seed, global row b, t, c), so a row's
+// values do not depend on how the batch is sharded. (Mirrors the reference's
+// make_bench_paths distribution, bench.cpp:134-161; the stream itself differs.)
+__device__ __forceinline__ void philox4x32_10(uint32_t (&ctr)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * ctr[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * ctr[2];
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        const uint32_t n0 = hi1 ^ ctr[1] ^ k0;
+        const uint32_t n2 = hi0 ^ ctr[3] ^ k1;
+        ctr[0] = n0;
+        ctr[1] = lo1;
+        ctr[2] = n2;
+        ctr[3] = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+template <typename Real>
+__global__ void brownian_kernel(Real* __restrict__ X, int64_t B, int64_t L, int d, uint64_t seed, int64_t row0) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (b, c)
+    if (i >= B * d) return;
+    const int64_t b = i / d;
+    const int c = (int)(i % d);
+    const int64_t gb = row0 + b;
+    const double sigma = L > 1 ? 1.0 / sqrt((double)(L - 1)) : 1.0;
+    Real* row = X + b * L * d + c;
+    double acc = 0.0;
+    row[0] = Real(0);
+    for (int64_t t = 1; t < L; ++t) {
+        uint32_t ctr[4] = {(uint32_t)t, (uint32_t)(t >> 32) ^ ((uint32_t)c << 16), (uint32_t)gb, (uint32_t)(gb >> 32)};
+        philox4x32_10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32));
+        const double u1 = ((double)ctr[0] + 1.0) * (1.0 / 4294967296.0);  // (0, 1]
+        const double u2 = (double)ctr[1] * (1.0 / 4294967296.0);
+        const double z = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+        acc += sigma * z;
+        row[t * d] = Real(acc);
+    }
+}
+
+}  // namespace sigk

@@ -1,0 +1,228 @@
+// C++ drop-in API (include/sigkit/*.hpp) over the C ABI (include/sigk.h).
+//
+// Mirrors the reference public surface (/root/reference/proj/src/kernels.cpp,
+// src/tensor_algebra.cpp): same validation messages and exception classes,
+// same layouts. Compute goes to the GPU through sigk_signature_f64/_f32.
+#include <cstdlib>
+#include <string>
+
+#include "sigk.h"
+#include "sigkit/kernels.hpp"
+#include "sigkit/tensor_algebra.hpp"
+
+namespace sigkit {
+
+namespace {
+
+[[noreturn]] void rethrow(int rc) {
+    const std::string msg = sigk_last_error();
+    if (rc == SIGK_EDOMAIN) throw DomainError(msg);
+    if (rc == SIGK_ERESOURCE) throw ResourceError(msg);
+    throw DeviceError(msg);
+}
+
+void check(int rc) {
+    if (rc != SIGK_OK) rethrow(rc);
+}
+
+// kernels.cpp:13-26 — identical checks and messages.
+void validate_paths(const PathBatch& p) {
+    if (p.batch < 1 || p.len < 1 || p.dim < 1) throw DomainError("paths: batch, len and dim must all be >= 1");
+    const std::size_t expected = p.batch * p.len * static_cast<std::size_t>(p.dim);
+    if (p.values.size() != expected)
+        throw DomainError("paths: values has " + std::to_string(p.values.size()) + " entries, shape implies " +
+                          std::to_string(expected));
+}
+
+void validate_depth(int depth) {
+    if (depth < 1) throw DomainError("depth must be >= 1, got " + std::to_string(depth));
+}
+
+SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats) {
+    validate_paths(paths);
+    validate_depth(depth);
+    SignatureBatch out;
+    out.batch = paths.batch;
+    out.dim = paths.dim;
+    out.depth = depth;
+    out.flat.resize(paths.batch * sig_dim(paths.dim, depth));
+    sigk_stats st{};
+    check(sigk_signature_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, out.flat.data(), 0u,
+                             nullptr, nullptr, &st));
+    if (stats) {
+        stats->fold_steps = st.fold_steps;
+        stats->scan_passes = st.scan_passes;
+    }
+    return out;
+}
+
+}  // namespace
+
+std::vector<double> SignatureBatch::row(std::size_t b) const {
+    const std::size_t w = width();
+    return std::vector<double>(flat.begin() + static_cast<std::ptrdiff_t>(b * w),
+                               flat.begin() + static_cast<std::ptrdiff_t>((b + 1) * w));
+}
+
+std::size_t PrefixSignatureBatch::width() const {
+    const std::size_t rows = batch * prefixes;
+    return rows == 0 ? 0 : flat.size() / rows;
+}
+
+std::vector<double> PrefixSignatureBatch::row(std::size_t b, std::size_t k) const {
+    const std::size_t w = width();
+    const std::size_t s = (b * prefixes + k) * w;
+    return std::vector<double>(flat.begin() + static_cast<std::ptrdiff_t>(s),
+                               flat.begin() + static_cast<std::ptrdiff_t>(s + w));
+}
+
+const char* kernel_name(KernelKind kind) {
+    switch (kind) {
+        case KernelKind::Sequential: return "sequential";
+        case KernelKind::Parallel: return "parallel";
+        case KernelKind::Auto: return "auto";
+    }
+    return "unknown";
+}
+
+KernelKind kernel_from_name(const std::string& name) {
+    if (name == "sequential") return KernelKind::Sequential;
+    if (name == "parallel") return KernelKind::Parallel;
+    if (name == "auto") return KernelKind::Auto;
+    throw DomainError("unknown kernel '" + name + "', expected sequential, parallel or auto");
+}
+
+ExecutionCaps ExecutionCaps::detect() {
+    ExecutionCaps caps;
+    const char* env = std::getenv("SIGKIT_ACCELERATED");
+    caps.accelerated = env == nullptr || (std::string(env) != "0");
+    return caps;
+}
+
+KernelKind select_kernel(KernelKind hint, const ExecutionCaps& caps, std::size_t seq_len) {
+    if (hint != KernelKind::Auto) return hint;
+    return (caps.accelerated && seq_len >= caps.parallel_min_len) ? KernelKind::Parallel : KernelKind::Sequential;
+}
+
+SignatureBatch signature_sequential(const PathBatch& paths, int depth, KernelStats* stats) {
+    return run_gpu(paths, depth, stats);
+}
+
+SignatureBatch signature_parallel(const PathBatch& paths, int depth, KernelStats* stats, std::size_t memory_cap) {
+    validate_paths(paths);
+    validate_depth(depth);
+    // Keep the reference's observable refusal (sig_core.hpp:161-173) so callers
+    // that rely on it behave the same; the GPU path itself has no such limit.
+    long double scalars = static_cast<long double>(paths.batch) * static_cast<long double>(paths.len);
+    for (int n = 0; n < depth; ++n) scalars *= static_cast<long double>(paths.dim);
+    if (scalars > static_cast<long double>(memory_cap))
+        throw ResourceError("parallel kernel: intermediate storage of ~" + std::to_string(static_cast<double>(scalars)) +
+                            " scalars exceeds cap " + std::to_string(memory_cap) +
+                            "; use the sequential kernel for this shape");
+    return run_gpu(paths, depth, stats);
+}
+
+SignatureBatch signature(const PathBatch& paths, int depth, KernelKind kernel, const ExecutionCaps& caps,
+                         KernelStats* stats) {
+    validate_paths(paths);
+    (void)select_kernel(kernel, caps, paths.len);
+    return run_gpu(paths, depth, stats);
+}
+
+void signature_f32(const float* paths, std::size_t batch, std::size_t len, int dim, int depth, float* out,
+                   KernelStats* stats) {
+    sigk_stats st{};
+    check(sigk_signature_f32(paths, batch, len, dim, depth, out, 0u, nullptr, nullptr, &st));
+    if (stats) {
+        stats->fold_steps = st.fold_steps;
+        stats->scan_passes = st.scan_passes;
+    }
+}
+
+// ---- tensor algebra (host utilities; semantics of tensor_algebra.cpp:10-127)
+
+std::size_t sig_dim(int dim, int depth) {
+    std::size_t D = 0;
+    check(sigk_sig_dim(dim, depth, &D));
+    return D;
+}
+
+std::vector<std::size_t> level_sizes(int dim, int depth) {
+    const auto off = level_offsets(dim, depth);
+    std::vector<std::size_t> s(static_cast<std::size_t>(depth));
+    for (int n = 0; n < depth; ++n) s[static_cast<std::size_t>(n)] = off[n + 1] - off[n];
+    return s;
+}
+
+std::vector<std::size_t> level_offsets(int dim, int depth) {
+    std::vector<std::size_t> off(static_cast<std::size_t>(depth > 0 ? depth + 1 : 1));
+    check(sigk_level_offsets(dim, depth, off.data()));
+    return off;
+}
+
+TruncatedTensor TruncatedTensor::zero(int dim, int depth) {
+    TruncatedTensor t;
+    t.dim = dim;
+    t.depth = depth;
+    for (std::size_t sz : level_sizes(dim, depth)) t.levels.emplace_back(sz, 0.0);
+    return t;
+}
+
+std::vector<double> tensor_product(const std::vector<double>& a, const std::vector<double>& b) {
+    std::vector<double> out;
+    out.reserve(a.size() * b.size());
+    for (double x : a)
+        for (double y : b) out.push_back(x * y);
+    return out;
+}
+
+TruncatedTensor restricted_exp(const std::vector<double>& v, int depth) {
+    if (v.empty()) throw DomainError("restricted_exp: empty increment");
+    TruncatedTensor t = TruncatedTensor::zero(static_cast<int>(v.size()), depth);
+    t.level(1) = v;
+    for (int n = 2; n <= depth; ++n) {
+        std::vector<double>& cur = t.level(n);
+        const std::vector<double>& prev = t.level(n - 1);
+        const double inv = 1.0 / n;
+        std::size_t w = 0;
+        for (double p : prev)
+            for (double x : v) cur[w++] = p * x * inv;
+    }
+    return t;
+}
+
+TruncatedTensor chen_product(const TruncatedTensor& a, const TruncatedTensor& b) {
+    if (a.dim != b.dim || a.depth != b.depth) throw DomainError("chen_product: operands must share dim and depth");
+    TruncatedTensor c = TruncatedTensor::zero(a.dim, a.depth);
+    for (int n = 1; n <= a.depth; ++n) {
+        std::vector<double>& cn = c.level(n);
+        for (std::size_t i = 0; i < cn.size(); ++i) cn[i] = a.level(n)[i] + b.level(n)[i];
+        for (int i = 1; i < n; ++i) {
+            const std::vector<double>& ai = a.level(i);
+            const std::vector<double>& bj = b.level(n - i);
+            std::size_t w = 0;
+            for (double x : ai)
+                for (double y : bj) cn[w++] += x * y;
+        }
+    }
+    return c;
+}
+
+FlatSignature flatten(const TruncatedTensor& t) {
+    FlatSignature f{t.dim, t.depth, {}};
+    for (const auto& l : t.levels) f.coeffs.insert(f.coeffs.end(), l.begin(), l.end());
+    return f;
+}
+
+TruncatedTensor unflatten(const FlatSignature& f) {
+    if (f.coeffs.size() != sig_dim(f.dim, f.depth))
+        throw DomainError("unflatten: coeffs length " + std::to_string(f.coeffs.size()) + " does not match sig_dim(" +
+                          std::to_string(f.dim) + ", " + std::to_string(f.depth) + ")");
+    TruncatedTensor t = TruncatedTensor::zero(f.dim, f.depth);
+    std::size_t w = 0;
+    for (auto& l : t.levels)
+        for (double& x : l) x = f.coeffs[w++];
+    return t;
+}
+
+}  // namespace sigkit
