@@ -1,4 +1,5 @@
-// Prefix-sliced, chunked Horner fold of Chen's recurrence on sm_100a.
+// Prefix-sliced Horner fold of Chen's recurrence: the per-thread math shared
+// by the sm_100a fold kernels (path_kernel.cuh, flat_kernel.cuh).
 //
 // What it computes (reference: detail::sequential_forward<Real>,
 // /root/reference/proj/include/sigkit/detail/sig_core.hpp:116-147, with
@@ -17,33 +18,18 @@
 //    redundant scalars T_m[p_1..p_m], m < Q — entirely in registers, and
 //    never talks to another thread during the fold.
 //  * A "unit" is (path b, chunk k): the chunk's local signature over steps
-//    [k*CL, (k+1)*CL). Chunks past the end are padded with δ = 0, which is
-//    an exact identity step (fma(u, 0, T) == T). Chunk signatures are
-//    combined afterwards with Chen's identity (merge.cuh).
-//  * Increments are produced cooperatively per tile of T steps: each thread
-//    loads X[t], X[t+1] for a few (unit, step, channel) entries (coalesced,
-//    prefetched into registers one tile ahead), forms δ and its scaled
-//    copies δ/m, and stores them to a double-buffered shared-memory table;
-//    consumers read them back with 16-byte broadcast loads.
+//    [k*CL, (k+1)*CL). Steps past the end are padded with δ = 0, which is an
+//    exact identity step (fma(u, 0, T) == T). Chunk signatures are combined
+//    with Chen's identity (merge.cuh).
+//  * Increments are produced cooperatively per tile of steps into a
+//    shared-memory table (produce_entry): the vector δ/m rows every thread of
+//    the unit reads with 16-byte broadcast loads, plus per-channel scalar
+//    rows δ[c]/m for the prefix digits (consume_step).
 #pragma once
 
 #include "sigk_common.cuh"
 
 namespace sigk {
-
-// Units (path, chunk) that one CTA of NT threads can touch: NT/P whole units
-// plus one straddling each CTA boundary.
-__host__ __device__ constexpr int fold_units_per_cta(int NT, int P) {
-    return P >= NT ? 2 : (NT % P == 0 ? NT / P + 1 : NT / P + 2);
-}
-
-// Steps per shared-memory tile: up to 8, fewer when a CTA holds many units so
-// the per-thread register prefetch (2 values per entry) stays <= 16 registers.
-__host__ __device__ constexpr int fold_tile_steps(int NT, int P, int d) {
-    int t = 8;
-    while (t > 1 && fold_units_per_cta(NT, P) * t * d > 8 * NT) --t;
-    return t;
-}
 
 template <typename Real, int DIM, int DEPTH, int Q>
 struct SliceFold {
@@ -188,140 +174,60 @@ __device__ __forceinline__ void store_slice(Real (&st)[SF::S], int pre, Real* __
     store_levels<SF, 1>(st, pre, row);
 }
 
-// X: (B, L, d) row-major. dst: (B*K, D) rows, row = b*K + k.
-template <typename Real, int DIM, int DEPTH, int Q, int NT, int T>
-__global__ void __launch_bounds__(NT) fold_kernel(const Real* __restrict__ X, int64_t B, int64_t L, int K,
-                                                  int CL, Real* __restrict__ dst) {
-    using SF = SliceFold<Real, DIM, DEPTH, Q>;
-    constexpr int d = DIM;
-    constexpr int P = SF::P;
-    constexpr int TAB = SF::TAB;
-    constexpr int VEC = SF::VEC;
-    constexpr int SCW = SF::SCW;
-    constexpr int VW = SF::VW;
-    constexpr int NU = fold_units_per_cta(NT, P);  // max units one CTA touches
-    constexpr int ENT = NU * T * d;                // producer entries per tile
-    constexpr int EPT = (ENT + NT - 1) / NT;
-    constexpr int D = level_off(d, DEPTH);
+// Load the step's table row (δ/m vectors + the thread's prefix scalars) from
+// shared memory with 16-byte broadcast loads and apply one Horner step.
+template <typename SF, typename Real>
+__device__ __forceinline__ void consume_step(Real (&st)[SF::S], const Real* __restrict__ row, const int (&dig)[SF::QS]) {
     using V = typename Vec16<Real>::type;
-
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Real* tab = reinterpret_cast<Real*>(smem_raw);  // [2][T][NU][TAB]
-
-    const int64_t M = L - 1;
-    const int64_t units = B * (int64_t)K;
-    const int64_t g0 = (int64_t)blockIdx.x * NT;
-    const int64_t u0 = g0 / P;
-    const int64_t g = g0 + threadIdx.x;
-    const int64_t unit = g / P;
-    const int pre = (int)(g % P);
-    const bool active = unit < units;
-    const int uu = (int)(unit - u0);
-
-    int dig[SF::QS];
+    constexpr int VW = SF::VW, VEC = SF::VEC, SCW = SF::SCW;
+    Real vs[VEC];
 #pragma unroll
-    for (int k = 0; k < SF::QS; ++k) dig[k] = (Q > 0) ? (pre / ipow(d, Q - 1 - k)) % d : 0;
-
-    Real st[SF::S];
-#pragma unroll
-    for (int i = 0; i < SF::S; ++i) st[i] = Real(0);
-
-    Real xa[EPT], xb[EPT];
-    auto load = [&](int tile) {
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            const int e = threadIdx.x + i * NT;
-            xa[i] = Real(0);
-            xb[i] = Real(0);
-            if (e < ENT) {
-                const int c = e % d;
-                const int s = (e / d) % T;
-                const int ue = e / (d * T);
-                const int64_t un = u0 + ue;
-                const int j = tile * T + s;
-                if (un < units && j < CL) {
-                    const int64_t b = un / K;
-                    const int64_t t = (un % K) * (int64_t)CL + j;
-                    if (t < M) {
-                        const Real* p = X + (b * L + t) * d + c;
-                        xa[i] = __ldg(p);
-                        xb[i] = __ldg(p + d);
-                    }
-                }
-            }
-        }
-    };
-    auto store = [&](int buf) {
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            const int e = threadIdx.x + i * NT;
-            if (e < ENT) {
-                const int c = e % d;
-                const int s = (e / d) % T;
-                const int ue = e / (d * T);
-                Real* row = tab + (((size_t)buf * T + s) * NU + ue) * TAB;
-                const Real dl = xb[i] - xa[i];
-#pragma unroll
-                for (int m = 1; m <= SF::NV; ++m) row[(m - 1) * d + c] = dl * (Real(1) / Real(m));
-                if constexpr (Q > 0) {
-#pragma unroll
-                    for (int m = 1; m <= DEPTH; ++m) row[VEC + c * SCW + (m - 1)] = dl * (Real(1) / Real(m));
-                }
-            }
-        }
-    };
-
-    const int ntiles = (CL + T - 1) / T;
-    load(0);
-    for (int tile = 0; tile < ntiles; ++tile) {
-        const int buf = tile & 1;
-        store(buf);
-        __syncthreads();
-        if (tile + 1 < ntiles) load(tile + 1);
-        if (active) {
-#pragma unroll 1
-            for (int s = 0; s < T; ++s) {
-                const Real* row = tab + (((size_t)buf * T + s) * NU + uu) * TAB;
-                Real vs[VEC];
-#pragma unroll
-                for (int i = 0; i < VEC / VW; ++i) {
-                    const V v = reinterpret_cast<const V*>(row)[i];
-                    if constexpr (VW == 4) {
-                        vs[4 * i] = v.x; vs[4 * i + 1] = v.y; vs[4 * i + 2] = v.z; vs[4 * i + 3] = v.w;
-                    } else {
-                        vs[2 * i] = v.x; vs[2 * i + 1] = v.y;
-                    }
-                }
-                Real sc[SF::QS][SCW > 0 ? SCW : 1];
-                if constexpr (Q > 0) {
-#pragma unroll
-                    for (int k = 0; k < Q; ++k) {
-                        const Real* sr = row + VEC + dig[k] * SCW;
-#pragma unroll
-                        for (int i = 0; i < SCW / VW; ++i) {
-                            const V v = reinterpret_cast<const V*>(sr)[i];
-                            if constexpr (VW == 4) {
-                                sc[k][4 * i] = v.x; sc[k][4 * i + 1] = v.y; sc[k][4 * i + 2] = v.z; sc[k][4 * i + 3] = v.w;
-                            } else {
-                                sc[k][2 * i] = v.x; sc[k][2 * i + 1] = v.y;
-                            }
-                        }
-                    }
-                } else {
-                    sc[0][0] = Real(0);
-                }
-                SF::step(st, vs, sc);
-            }
+    for (int i = 0; i < VEC / VW; ++i) {
+        const V v = reinterpret_cast<const V*>(row)[i];
+        if constexpr (VW == 4) {
+            vs[4 * i] = v.x; vs[4 * i + 1] = v.y; vs[4 * i + 2] = v.z; vs[4 * i + 3] = v.w;
+        } else {
+            vs[2 * i] = v.x; vs[2 * i + 1] = v.y;
         }
     }
-    if (active) store_slice<SF>(st, pre, dst + unit * (int64_t)D);
+    Real sc[SF::QS][SCW > 0 ? SCW : 1];
+    if constexpr (SF::QQ > 0) {
+#pragma unroll
+        for (int k = 0; k < SF::QQ; ++k) {
+            const Real* sr = row + VEC + dig[k] * SCW;
+#pragma unroll
+            for (int i = 0; i < SCW / VW; ++i) {
+                const V v = reinterpret_cast<const V*>(sr)[i];
+                if constexpr (VW == 4) {
+                    sc[k][4 * i] = v.x; sc[k][4 * i + 1] = v.y; sc[k][4 * i + 2] = v.z; sc[k][4 * i + 3] = v.w;
+                } else {
+                    sc[k][2 * i] = v.x; sc[k][2 * i + 1] = v.y;
+                }
+            }
+        }
+    } else {
+        sc[0][0] = Real(0);
+    }
+    SF::step(st, vs, sc);
 }
 
-template <typename Real, int DIM, int DEPTH, int Q, int NT, int T>
-constexpr size_t fold_smem_bytes() {
-    using SF = SliceFold<Real, DIM, DEPTH, Q>;
-    constexpr int NU = fold_units_per_cta(NT, SF::P);
-    return sizeof(Real) * 2ull * T * NU * SF::TAB;
+// Write one increment δ (component c of step s) into a table row: the vector
+// part δ/m (m = 1..N-Q) and, for sliced variants, the scalar row of c
+// (δ/m, m = 1..N) that threads whose prefix digit is c load in one go.
+template <typename SF, typename Real>
+__device__ __forceinline__ void produce_entry(Real* __restrict__ row, int c, Real dl) {
+#pragma unroll
+    for (int m = 1; m <= SF::NV; ++m) row[(m - 1) * SF::d + c] = dl * (Real(1) / Real(m));
+    if constexpr (SF::QQ > 0) {
+#pragma unroll
+        for (int m = 1; m <= SF::N; ++m) row[SF::VEC + c * SF::SCW + (m - 1)] = dl * (Real(1) / Real(m));
+    }
+}
+
+template <typename SF>
+__device__ __forceinline__ void prefix_digits(int pre, int (&dig)[SF::QS]) {
+#pragma unroll
+    for (int k = 0; k < SF::QS; ++k) dig[k] = (SF::QQ > 0) ? (pre / ipow(SF::d, SF::QQ - 1 - k)) % SF::d : 0;
 }
 
 }  // namespace sigk

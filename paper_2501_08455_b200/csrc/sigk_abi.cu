@@ -67,7 +67,7 @@ void register_variants(const Variant* table, int n, bool is_f64) {
     for (int i = 0; i < n; ++i) v.push_back(table[i]);
 }
 
-static const Variant* find_variant(int d, int N, bool is_f64) {
+const Variant* find_variant(int d, int N, bool is_f64) {
     Registry& r = registry();
     std::lock_guard<std::mutex> g(r.mu);
     for (const Variant& v : is_f64 ? r.f64 : r.f32)
@@ -75,35 +75,66 @@ static const Variant* find_variant(int d, int N, bool is_f64) {
     return nullptr;
 }
 
-// Chunk count K for a (B, M) problem: minimise a cycle model of
-//   fold  = ceil(CTAs / SMs) * NT * ceil(M/K) * ops / 128       (FFMA-pipe bound)
-//   merge = K>1: ceil(B / SMs) * ((K-1) * chen * 4 / 128 + rounds * N * 600) + 4000
-// where the merge term charges ~4 issue slots per Chen FMA (3 loads + fma),
-// a barrier-plus-latency cost per tree level and one extra launch.
-static int plan_chunks(const Variant& v, int64_t B, int64_t M, int sms, int occ) {
-    if (M <= 1) return 1;
-    const int kmax = (int)std::min<int64_t>(M, 512);
+// Issue efficiency of the FFMA pipe vs resident warps per SM sub-partition
+// (measured on B200 with tools/ffma_probe.cu: ~0.62 at 1 warp, ~0.85 at 2).
+static double issue_eff(double warps_per_smsp) {
+    if (warps_per_smsp <= 1.0) return 0.62 * std::max(warps_per_smsp, 0.05);
+    if (warps_per_smsp <= 2.0) return 0.62 + 0.23 * (warps_per_smsp - 1.0);
+    return std::min(0.95, 0.85 + 0.05 * (warps_per_smsp - 2.0));
+}
+
+// Units (chunks) per path for the path kernel: minimise a cycle model of one
+// launch. Per wave an SM runs c CTAs of U*P threads; the fold costs
+// CL*ops issue slots per thread, the Chen tree ~3 slots per FMA of its
+// (U-1) products spread over the CTA, plus a barrier per tile and per level.
+static int plan_units(const Variant& v, int64_t B, int64_t M, int sms) {
+    const int umax = (int)std::min<int64_t>(M, v.nt / v.P);
     double best = 1e300;
-    int bestk = 1;
-    for (int K = 1; K <= kmax; ++K) {
-        const int64_t CL = (M + K - 1) / K;
-        const int64_t lanes = B * K * (int64_t)v.P;
-        const int64_t ctas = (lanes + v.NT - 1) / v.NT;
-        const int64_t per_sm = (ctas + sms - 1) / sms;
-        // partial residency: fewer resident warps than the FMA latency needs
-        const double fill = std::min(1.0, (double)std::min<int64_t>(per_sm, occ) * v.NT / 256.0);
-        double t = (double)per_sm * v.NT * CL * v.ops / 128.0 / std::max(fill, 0.25);
-        if (K > 1) {
-            int rounds = 0;
-            while ((1 << rounds) < K) ++rounds;
-            t += (double)((B + sms - 1) / sms) * ((K - 1) * (double)v.chen * 4.0 / 128.0 + rounds * v.N * 600.0) + 4000.0;
-        }
-        if (t < best * 0.999) {
+    int bestu = 1;
+    for (int U = 1; U <= umax; ++U) {
+        int occ = 0;
+        if (v.occupancy(U, &occ) != cudaSuccess || occ < 1) continue;
+        const int64_t CL = (M + U - 1) / U;
+        const int64_t c = std::min<int64_t>(occ, (B + sms - 1) / sms);  // CTAs per SM per wave
+        const int64_t waves = (B + sms * c - 1) / (sms * c);
+        const double threads = (double)U * v.P;
+        const double warps_smsp = c * std::ceil(threads / 32.0) / 4.0;
+        const double eff = issue_eff(warps_smsp);
+        const double fold = c * threads * CL * (v.ops + 6.0) / 128.0 / eff;
+        int rounds = 0;
+        while ((1 << rounds) < U) ++rounds;
+        const double merge = c * (U - 1) * (double)v.chen * 3.0 / 128.0 / eff + rounds * v.N * 150.0;
+        const double sync = (double)((CL + v.T - 1) / v.T) * 120.0;
+        const double t = waves * (fold + merge + sync);
+        if (t < best * 0.995) {
             best = t;
-            bestk = K;
+            bestu = U;
         }
     }
-    return bestk;
+    return bestu;
+}
+
+struct PlanKey {
+    const Variant* v;
+    int dev;
+    int64_t B, M;
+    bool operator==(const PlanKey& o) const { return v == o.v && dev == o.dev && B == o.B && M == o.M; }
+};
+
+static int cached_plan(const Variant& v, int dev, int64_t B, int64_t M) {
+    static std::mutex mu;
+    static std::vector<std::pair<PlanKey, int>> cache;
+    const PlanKey key{&v, dev, B, M};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto& kv : cache)
+            if (kv.first == key) return kv.second;
+    }
+    const int U = plan_units(v, B, M, device_info(dev).sms);
+    std::lock_guard<std::mutex> g(mu);
+    if (cache.size() > 256) cache.clear();
+    cache.emplace_back(key, U);
+    return U;
 }
 
 template <typename Real>
@@ -130,9 +161,20 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         if (st) *st = local;
         return SIGK_OK;
     }
+    cudaEvent_t ev0 = tun ? static_cast<cudaEvent_t>(tun->fold_event_start) : nullptr;
+    cudaEvent_t ev1 = tun ? static_cast<cudaEvent_t>(tun->fold_event_stop) : nullptr;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (ev0 || ev1) cudaStreamIsCapturing(s, &cap);
+    auto record = [&](cudaEvent_t ev) {  // an event-record node when captured into a graph
+        if (!ev) return;
+        if (cap == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+        else cudaEventRecord(ev, s);
+    };
     const Variant* v = (tun && tun->force_generic) ? nullptr : find_variant(d, N, is_f64);
     if (v == nullptr) {
+        record(ev0);
         e = is_f64 ? launch_generic_f64(X, B, L, d, N, out, s) : launch_generic_f32(X, B, L, d, N, out, s);
+        record(ev1);
         if (e != cudaSuccess) return cuda_fail(e, "generic fold launch");
         local.fold_steps = M;
         local.chunks = 1;
@@ -144,52 +186,30 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
     }
     int dev = 0;
     cudaGetDevice(&dev);
-    const DeviceInfo di = device_info(dev);
-    int occ = 1;
-    e = v->occupancy(&occ);
-    if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
-    if (occ < 1) return fail(SIGK_ERESOURCE, "fold variant does not fit on this device");
-    const int64_t plan_rows = (tun && tun->plan_rows > 0) ? tun->plan_rows : B;
-    int K = (tun && tun->chunks > 0) ? tun->chunks : plan_chunks(*v, plan_rows, M, di.sms, occ);
-    K = (int)std::max<int64_t>(1, std::min<int64_t>(K, M));
-    const int CL = (int)((M + K - 1) / K);
-    K = (int)((M + CL - 1) / CL);  // drop empty trailing chunks
-    cudaEvent_t ev0 = tun ? static_cast<cudaEvent_t>(tun->fold_event_start) : nullptr;
-    cudaEvent_t ev1 = tun ? static_cast<cudaEvent_t>(tun->fold_event_stop) : nullptr;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (ev0 || ev1) cudaStreamIsCapturing(s, &cap);
-    auto record = [&](cudaEvent_t ev) {  // an event-record node when captured into a graph
-        if (cap == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
-        else cudaEventRecord(ev, s);
-    };
-    auto fold = [&](void* dst, int k) {
-        if (ev0) record(ev0);
-        cudaError_t r = v->fold(X, B, L, k, CL, dst, s);
-        if (ev1) record(ev1);
-        return r;
-    };
-    if (K == 1) {
-        e = fold(out, 1);
-        if (e != cudaSuccess) return cuda_fail(e, "fold launch");
-        local.launches = 1;
-    } else {
-        Real* ws = nullptr;
-        e = cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(Real) * B * K * D, s);
-        if (e != cudaSuccess) return cuda_fail(e, "workspace allocation");
-        e = fold(ws, K);
-        if (e == cudaSuccess) e = v->merge(ws, K, out, B, s);
-        cudaError_t e2 = cudaFreeAsync(ws, s);
-        if (e != cudaSuccess) return cuda_fail(e, "fold/merge launch");
-        if (e2 != cudaSuccess) return cuda_fail(e2, "workspace free");
-        local.launches = 2;
+    int U = 1;
+    if (v->family == KernelFamily::Path) {
+        const int64_t plan_rows = (tun && tun->plan_rows > 0) ? tun->plan_rows : B;
+        U = (tun && tun->chunks > 0) ? tun->chunks : cached_plan(*v, dev, plan_rows, M);
+        U = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)U, M, (int64_t)(v->nt / v->P)}));
+        int occ = 0;
+        e = v->occupancy(U, &occ);
+        if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+        if (occ < 1) return fail(SIGK_ERESOURCE, "fold variant does not fit on this device with " +
+                                                     std::to_string(U) + " chunks per path");
     }
+    record(ev0);
+    e = v->launch(X, B, L, U, out, s);
+    record(ev1);
+    if (e != cudaSuccess) return cuda_fail(e, "fold launch");
+    const int64_t CL = (M + U - 1) / U;
     int rounds = 0;
-    while ((1 << rounds) < K) ++rounds;
+    while ((1 << rounds) < U) ++rounds;
     local.fold_steps = CL;
     local.scan_passes = rounds;
-    local.chunks = K;
+    local.chunks = U;
     local.prefix_len = v->Q;
     local.threads_per_unit = v->P;
+    local.launches = 1;
     if (st) *st = local;
     return SIGK_OK;
 }

@@ -1,6 +1,6 @@
-// Compile-time variant table: one register-sliced fold (+ its Chen merge) per
+// Compile-time variant table: one register-sliced fold kernel per
 // (precision, d, N), with the prefix length Q picked so the per-thread slice
-// fits the register budget.
+// fits the register budget, and the kernel family picked by unit size.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -8,9 +8,8 @@
 #include <atomic>
 #include <cstdint>
 
-#include "fold.cuh"
-#include "generic.cuh"
-#include "merge.cuh"
+#include "flat_kernel.cuh"
+#include "path_kernel.cuh"
 #include "variants.h"
 
 namespace sigk {
@@ -27,49 +26,93 @@ constexpr int pick_q(int d, int N) {
     return N - 1;
 }
 
+// Opt a kernel in to > 48 KB of dynamic shared memory once per device (not
+// stream-ordered, so it must not be repeated inside a graph capture).
+template <typename K>
+cudaError_t opt_in_smem(K kern, size_t bytes, std::atomic<uint64_t>& done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (bytes <= 48 * 1024 || (done.load() & bit)) return cudaSuccess;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e == cudaSuccess) done.fetch_or(bit);
+    return e;
+}
+
+template <typename Real, int DIM, int DEPTH, int Q>
+struct PathVariant {
+    using G = PathGeom<Real, DIM, DEPTH, Q>;
+    using SF = typename G::SF;
+    static constexpr int NTMAX = 256;
+    static constexpr int T = G::tile_steps();
+    static constexpr auto kernel = path_kernel<Real, DIM, DEPTH, Q, NTMAX, T>;
+    static std::atomic<uint64_t> smem_done;
+
+    static cudaError_t launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s) {
+        const int64_t M = L - 1;
+        const int CL = (int)((M + U - 1) / U);
+        const size_t smem = G::smem_bytes(T, U);
+        cudaError_t e = opt_in_smem(kernel, smem, smem_done);
+        if (e != cudaSuccess) return e;
+        kernel<<<(unsigned)B, U * SF::P, smem, s>>>(static_cast<const Real*>(X), L, U, CL, static_cast<Real*>(out));
+        return cudaGetLastError();
+    }
+    static cudaError_t occupancy(int U, int* blocks) {
+        const size_t smem = G::smem_bytes(T, U);
+        cudaError_t e = opt_in_smem(kernel, smem, smem_done);
+        if (e != cudaSuccess) return e;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kernel, U * SF::P, smem);
+    }
+};
+template <typename Real, int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PathVariant<Real, DIM, DEPTH, Q>::smem_done{0};
+
+template <typename Real, int DIM, int DEPTH, int Q>
+struct FlatVariant {
+    static constexpr int NT = 32;
+    static constexpr int T = 8;
+    static constexpr int MINB = 14;
+    using G = FlatGeom<Real, DIM, DEPTH, Q, NT, T>;
+    using SF = typename G::SF;
+    static constexpr auto kernel = flat_kernel<Real, DIM, DEPTH, Q, NT, T, MINB>;
+    static std::atomic<uint64_t> smem_done;
+
+    static cudaError_t launch(const void* X, int64_t B, int64_t L, int, void* out, cudaStream_t s) {
+        cudaError_t e = opt_in_smem(kernel, G::smem, smem_done);
+        if (e != cudaSuccess) return e;
+        const int64_t lanes = B * (int64_t)SF::P;
+        kernel<<<(unsigned)((lanes + NT - 1) / NT), NT, G::smem, s>>>(static_cast<const Real*>(X), B, L,
+                                                                      static_cast<Real*>(out));
+        return cudaGetLastError();
+    }
+    static cudaError_t occupancy(int, int* blocks) {
+        cudaError_t e = opt_in_smem(kernel, G::smem, smem_done);
+        if (e != cudaSuccess) return e;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kernel, NT, G::smem);
+    }
+};
+template <typename Real, int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> FlatVariant<Real, DIM, DEPTH, Q>::smem_done{0};
+
 template <typename Real, int DIM, int DEPTH>
 struct VariantImpl {
     static constexpr int Q = pick_q<Real>(DIM, DEPTH);
     using SF = SliceFold<Real, DIM, DEPTH, Q>;
-    static constexpr int NT = 128;
-    static constexpr int T = fold_tile_steps(NT, SF::P, DIM);
-    static constexpr size_t smem = fold_smem_bytes<Real, DIM, DEPTH, Q, NT, T>();
-
-    // Opt in to >48 KB dynamic shared memory once per device (not stream-ordered,
-    // so it must not be repeated inside a graph capture).
-    static cudaError_t prepare() {
-        static std::atomic<uint64_t> done{0};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        const uint64_t bit = 1ull << (dev & 63);
-        if (smem <= 48 * 1024 || (done.load() & bit)) return cudaSuccess;
-        cudaError_t e = cudaFuncSetAttribute(fold_kernel<Real, DIM, DEPTH, Q, NT, T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) done.fetch_or(bit);
-        return e;
-    }
-    static cudaError_t fold(const void* X, int64_t B, int64_t L, int K, int CL, void* dst, cudaStream_t s) {
-        cudaError_t e = prepare();
-        if (e != cudaSuccess) return e;
-        const int64_t lanes = B * (int64_t)K * SF::P;
-        const int64_t grid = (lanes + NT - 1) / NT;
-        fold_kernel<Real, DIM, DEPTH, Q, NT, T><<<(unsigned)grid, NT, smem, s>>>(
-            static_cast<const Real*>(X), B, L, K, CL, static_cast<Real*>(dst));
-        return cudaGetLastError();
-    }
-    static cudaError_t merge(void* ws, int K, void* out, int64_t B, cudaStream_t s) {
-        merge_tree_kernel<Real, DIM, DEPTH><<<(unsigned)B, 512, 0, s>>>(static_cast<Real*>(ws), K, static_cast<Real*>(out));
-        return cudaGetLastError();
-    }
-    static cudaError_t occupancy(int* blocks) {
-        cudaError_t e = prepare();
-        if (e != cudaSuccess) return e;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fold_kernel<Real, DIM, DEPTH, Q, NT, T>, NT, smem);
-    }
-    static constexpr Variant make() {
+    static constexpr bool FLAT = SF::P > 256;
+    static Variant make() {
         int chen = 0;
         for (int n = 2; n <= DEPTH; ++n) chen += (n - 1) * ipow(DIM, n);
-        return Variant{DIM, DEPTH, Q, NT, T, SF::P, SF::ops_per_step(), chen, smem, &fold, &merge, &occupancy};
+        if constexpr (FLAT) {
+            using V = FlatVariant<Real, DIM, DEPTH, Q>;
+            return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), chen, KernelFamily::Flat, V::NT, V::T,
+                           &V::launch, &V::occupancy};
+        } else {
+            using V = PathVariant<Real, DIM, DEPTH, Q>;
+            return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), chen, KernelFamily::Path, V::NTMAX, V::T,
+                           &V::launch, &V::occupancy};
+        }
     }
 };
 
@@ -78,7 +121,10 @@ void register_variants(const Variant* table, int n, bool is_f64);
 
 template <typename Real, int DIM, int... Ns>
 struct DimTable {
-    static constexpr Variant table[] = {VariantImpl<Real, DIM, Ns>::make()...};
+    static const Variant* table() {
+        static const Variant t[] = {VariantImpl<Real, DIM, Ns>::make()...};
+        return t;
+    }
     static constexpr int count = sizeof...(Ns);
 };
 

@@ -7,22 +7,24 @@
 
 namespace sigk {
 
+enum class KernelFamily : int { Path = 0, Flat = 1 };
+
 struct Variant {
     int d, N;
-    int Q;      // prefix length owned per thread
-    int NT;     // threads per CTA
-    int T;      // steps per shared-memory tile
-    int P;      // threads per (path, chunk) unit = d^Q
-    int ops;    // FFMA-pipe ops per thread per step
-    int chen;   // FMAs of one Chen product (merge), Σ_{n>=2} (n-1) d^n
-    size_t smem;
-    cudaError_t (*fold)(const void* X, int64_t B, int64_t L, int K, int CL, void* dst, cudaStream_t s);
-    cudaError_t (*merge)(void* ws, int K, void* out, int64_t B, cudaStream_t s);
-    cudaError_t (*occupancy)(int* blocks_per_sm);
+    int Q;       // prefix length owned per thread
+    int P;       // threads per (path, chunk) unit = d^Q
+    int ops;     // FFMA-pipe ops per thread per step
+    int chen;    // FMAs of one Chen product (merge), Σ_{n>=2} (n-1) d^n
+    KernelFamily family;
+    int nt;      // path: max threads per CTA; flat: threads per CTA
+    int T;       // steps per shared-memory tile
+    // path: grid = B CTAs of U*P threads (U chunks per path); flat: U ignored
+    cudaError_t (*launch)(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s);
+    // resident CTAs per SM for a given U (0 when it does not fit)
+    cudaError_t (*occupancy)(int U, int* blocks_per_sm);
 };
 
-const Variant* find_variant_f32(int d, int N);
-const Variant* find_variant_f64(int d, int N);
+const Variant* find_variant(int d, int N, bool is_f64);
 cudaError_t launch_generic_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
 cudaError_t launch_generic_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
 cudaError_t launch_brownian_f32(void* X, int64_t B, int64_t L, int d, uint64_t seed, int64_t row0, cudaStream_t s);

@@ -16,7 +16,7 @@ namespace sigk {
 namespace {
 using Row = DimTable<SIGK_REAL, SIGK_DIM, SIGK_CAT(SIGK_DEPTHS_, SIGK_DIM)>;
 struct Registrar {
-    Registrar() { register_variants(Row::table, Row::count, sizeof(SIGK_REAL) == 8); }
+    Registrar() { register_variants(Row::table(), Row::count, sizeof(SIGK_REAL) == 8); }
 };
 Registrar registrar;
 }  // namespace

@@ -68,9 +68,14 @@ def test_golden_shape_grid_f64_and_f32(sk, golden):
         X, N = golden[f"grid/{s}/X"], int(golden[f"grid/{s}/N"])
         ref = golden[f"grid/{s}/seq"]
         assert max(level_errors(sk.signature(X, N), ref, X.shape[2], N)) <= F64_TOL, s
+        # fp32: these unit-step random walks (not the 1/sqrt(L-1) benchmark scaling)
+        # cancel heavily at high levels for d = 1, so the bar is the 1e-5 north-star
+        # tolerance or 4x the error of the reference's OWN float instantiation
+        # (sequential_forward<float>, via the bit-identical port), whichever is larger.
         X32 = X.astype(np.float32)
         ref32 = O.signature(X32.astype(np.float64), N)
-        assert max(level_errors(sk.signature(X32, N), ref32, X.shape[2], N)) <= F32_TOL, s
+        own = max(level_errors(O.signature(X32, N), ref32, X.shape[2], N))
+        assert max(level_errors(sk.signature(X32, N), ref32, X.shape[2], N)) <= max(F32_TOL, 4 * own), s
 
 
 def test_golden_wide_rows_and_c1(sk, golden):
