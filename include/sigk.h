@@ -81,7 +81,8 @@ typedef struct sigk_tuning {
     void* fold_event_start; /* optional cudaEvent_t recorded on the stream just
                                before the fold kernel (instrumentation) */
     void* fold_event_stop;  /* ... and just after it */
-    int32_t reserved[4];
+    int32_t prefix_len;     /* pin Q, the leading indices owned per thread (0: planned) */
+    int32_t reserved[3];
 } sigk_tuning;
 
 int sigk_sig_dim(int d, int N, size_t* D);

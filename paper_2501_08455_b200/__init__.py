@@ -48,7 +48,8 @@ class _Stats(C.Structure):
 
 class _Tuning(C.Structure):
     _fields_ = [("chunks", C.c_int32), ("force_generic", C.c_int32), ("plan_rows", C.c_int64),
-                ("fold_event_start", C.c_void_p), ("fold_event_stop", C.c_void_p), ("reserved", C.c_int32 * 4)]
+                ("fold_event_start", C.c_void_p), ("fold_event_stop", C.c_void_p), ("prefix_len", C.c_int32),
+                ("reserved", C.c_int32 * 3)]
 
 
 @dataclass
@@ -178,9 +179,9 @@ def _validate_shape(shape, depth):
 
 
 def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_generic: bool = False,
-         out=None, plan_rows: int = 0):
+         out=None, plan_rows: int = 0, prefix_len: int = 0):
     st = _Stats()
-    tun = _Tuning(chunks=chunks, force_generic=int(force_generic), plan_rows=plan_rows)
+    tun = _Tuning(chunks=chunks, force_generic=int(force_generic), plan_rows=plan_rows, prefix_len=prefix_len)
     if _is_torch(paths):
         import torch
 
@@ -215,7 +216,8 @@ def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_ge
 
 
 def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
-              stats: KernelStats | None = None, *, chunks: int = 0, out=None, plan_rows: int = 0):
+              stats: KernelStats | None = None, *, chunks: int = 0, out=None, plan_rows: int = 0,
+              prefix_len: int = 0):
     """Reference ``sigkit::signature`` (kernels.cpp:200-206): (B, L, d) -> (B, D).
 
     ``kernel``/``caps`` are accepted for source compatibility; every kind runs
@@ -224,7 +226,7 @@ def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: Exe
     are bitwise independent of batch composition at equal chunking).
     """
     select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
-    return _run(paths, depth, stats, chunks=chunks, out=out, plan_rows=plan_rows)
+    return _run(paths, depth, stats, chunks=chunks, out=out, plan_rows=plan_rows, prefix_len=prefix_len)
 
 
 def signature_sequential(paths, depth: int, stats: KernelStats | None = None, **kw):

@@ -10,9 +10,11 @@
 // independent of the launch shape. Each product overwrites its left operand
 // one level at a time in DESCENDING order with a CTA barrier between levels:
 // level n reads only levels < n of A, which are still intact. Inside a level
-// every output element is independent, so all threads of the CTA share the
-// work of every pair of the round (prefix index I / d^(n-i) into A_i, suffix
-// index I mod d^(n-i) into B_{n-i}; divisors are compile-time).
+// the work is split into runs of d consecutive outputs I = R*d + c (last index
+// varying): the whole run shares every prefix A_i[R / d^(n-i-1)] (one load
+// each) and reads contiguous suffix runs B_{n-i}[(R mod d^(n-i-1))*d + c], so
+// a run costs (n+1)d + n-1 loads for (n-1)d FMAs; all threads of the CTA share
+// the runs of every pair of the round. Divisors are compile-time.
 #pragma once
 
 #include "sigk_common.cuh"
@@ -20,28 +22,35 @@
 namespace sigk {
 
 template <typename Real, int d, int n, int i>
-__device__ __forceinline__ void chen_terms(const Real* __restrict__ A, const Real* __restrict__ Bm, int I, Real& acc) {
+__device__ __forceinline__ void chen_run_terms(const Real* __restrict__ A, const Real* __restrict__ Bm, int R,
+                                               Real (&acc)[d]) {
     if constexpr (i < n) {
-        constexpr int tail = ipow(d, n - i);
-        acc = fma(A[level_off(d, i - 1) + I / tail], Bm[level_off(d, n - i - 1) + I % tail], acc);
-        chen_terms<Real, d, n, i + 1>(A, Bm, I, acc);
+        constexpr int tail = ipow(d, n - i - 1);  // I / d^(n-i) = R / tail
+        const Real a = A[level_off(d, i - 1) + R / tail];
+        const Real* __restrict__ br = Bm + level_off(d, n - i - 1) + (R % tail) * d;
+#pragma unroll
+        for (int c = 0; c < d; ++c) acc[c] = fma(a, br[c], acc[c]);
+        chen_run_terms<Real, d, n, i + 1>(A, Bm, R, acc);
     }
 }
 
 template <typename Real, int d, int N, int n>
 __device__ __forceinline__ void merge_level_desc(Real* __restrict__ sig, int D, int h, int pairs) {
     if constexpr (n >= 1) {
-        constexpr int lsz = ipow(d, n);
+        constexpr int runs = ipow(d, n - 1);
         constexpr int o = level_off(d, n - 1);
-        const int work = pairs * lsz;
+        const int work = pairs * runs;
         for (int w = threadIdx.x; w < work; w += blockDim.x) {
-            const int pj = w / lsz;
-            const int I = w - pj * lsz;
+            const int pj = w / runs;
+            const int R = w - pj * runs;
             Real* A = sig + (2 * h * pj) * D;
             const Real* Bm = A + h * D;
-            Real acc = A[o + I] + Bm[o + I];
-            chen_terms<Real, d, n, 1>(A, Bm, I, acc);
-            A[o + I] = acc;
+            Real acc[d];
+#pragma unroll
+            for (int c = 0; c < d; ++c) acc[c] = A[o + R * d + c] + Bm[o + R * d + c];
+            chen_run_terms<Real, d, n, 1>(A, Bm, R, acc);
+#pragma unroll
+            for (int c = 0; c < d; ++c) A[o + R * d + c] = acc[c];
         }
         __syncthreads();
         merge_level_desc<Real, d, N, n - 1>(sig, D, h, pairs);

@@ -70,9 +70,19 @@ void register_variants(const Variant* table, int n, bool is_f64) {
 const Variant* find_variant(int d, int N, bool is_f64) {
     Registry& r = registry();
     std::lock_guard<std::mutex> g(r.mu);
+    const Variant* best = nullptr;
     for (const Variant& v : is_f64 ? r.f64 : r.f32)
-        if (v.d == d && v.N == N) return &v;
-    return nullptr;
+        if (v.d == d && v.N == N && (!best || v.Q < best->Q)) best = &v;
+    return best;
+}
+
+int find_variants(int d, int N, bool is_f64, const Variant** out, int max) {
+    Registry& r = registry();
+    std::lock_guard<std::mutex> g(r.mu);
+    int n = 0;
+    for (const Variant& v : is_f64 ? r.f64 : r.f32)
+        if (v.d == d && v.N == N && n < max) out[n++] = &v;
+    return n;
 }
 
 // Issue efficiency of the FFMA pipe vs resident warps per SM sub-partition
@@ -83,58 +93,85 @@ static double issue_eff(double warps_per_smsp) {
     return std::min(0.95, 0.85 + 0.05 * (warps_per_smsp - 2.0));
 }
 
-// Units (chunks) per path for the path kernel: minimise a cycle model of one
-// launch. Per wave an SM runs c CTAs of U*P threads; the fold costs
-// CL*ops issue slots per thread, the Chen tree ~3 slots per FMA of its
-// (U-1) products spread over the CTA, plus a barrier per tile and per level.
-static int plan_units(const Variant& v, int64_t B, int64_t M, int sms) {
-    const int umax = (int)std::min<int64_t>(M, v.nt / v.P);
-    double best = 1e300;
-    int bestu = 1;
-    for (int U = 1; U <= umax; ++U) {
-        int occ = 0;
-        if (v.occupancy(U, &occ) != cudaSuccess || occ < 1) continue;
-        const int64_t CL = (M + U - 1) / U;
-        const int64_t c = std::min<int64_t>(occ, (B + sms - 1) / sms);  // CTAs per SM per wave
-        const int64_t waves = (B + sms * c - 1) / (sms * c);
-        const double threads = (double)U * v.P;
-        const double warps_smsp = c * std::ceil(threads / 32.0) / 4.0;
-        const double eff = issue_eff(warps_smsp);
-        const double fold = c * threads * CL * (v.ops + 6.0) / 128.0 / eff;
-        int rounds = 0;
-        while ((1 << rounds) < U) ++rounds;
-        const double merge = c * (U - 1) * (double)v.chen * 3.0 / 128.0 / eff + rounds * v.N * 150.0;
-        const double sync = (double)((CL + v.T - 1) / v.T) * 120.0;
-        const double t = waves * (fold + merge + sync);
-        if (t < best * 0.995) {
-            best = t;
-            bestu = U;
+// Cycle model of one launch (SM cycles). Path kernel: a wave puts c CTAs of
+// U*P threads on each SM; a thread issues CL * (ops + loads + producer + 2)
+// slots for the fold, the Chen tree issues ~12 slots per output element per
+// product ((U-1) products of D elements) plus barriers per level and round.
+static double model_cycles(const Variant& v, int64_t B, int64_t M, int sms, int U, int occ, int64_t D) {
+    const double prod = (double)((v.T * v.d + v.P - 1) / v.P) * (v.N + (v.N - v.Q) + 4) / v.T;
+    const double per_step = v.ops + v.loads + prod + 2.0;
+    if (v.family == KernelFamily::Flat) {
+        const int64_t ctas = (B * v.P + v.nt - 1) / v.nt;
+        const int64_t per_sm = (ctas + sms - 1) / sms;
+        const int64_t c = std::min<int64_t>(occ, per_sm);
+        const int64_t waves = (per_sm + c - 1) / c;
+        const double eff = issue_eff(c * (v.nt / 32.0) / 4.0);
+        return waves * (c * v.nt * (double)M * per_step / 128.0 / eff);
+    }
+    const int64_t CL = (M + U - 1) / U;
+    const int64_t c = std::min<int64_t>(occ, (B + sms - 1) / sms);  // CTAs per SM per wave
+    const int64_t waves = (B + sms * c - 1) / (sms * c);
+    const double threads = (double)U * v.P;
+    const double eff = issue_eff(c * std::ceil(threads / 32.0) / 4.0);
+    const double fold = c * threads * CL * per_step / 128.0 / eff;
+    int rounds = 0;
+    while ((1 << rounds) < U) ++rounds;
+    const double merge = c * (U - 1) * (double)D * 12.0 / 128.0 / eff + rounds * v.N * 120.0;
+    const double sync = (double)((CL + v.T - 1) / v.T) * 100.0;
+    return waves * (fold + merge + sync);
+}
+
+struct Plan {
+    const Variant* v = nullptr;
+    int U = 1;
+};
+
+// Pick the variant (prefix length Q) and chunks per path U for a launch.
+static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms, int64_t D) {
+    const Variant* cands[4];
+    const int nc = find_variants(d, N, is_f64, cands, 4);
+    Plan best;
+    double best_t = 1e300;
+    for (int k = 0; k < nc; ++k) {
+        const Variant& v = *cands[k];
+        const int umax = v.family == KernelFamily::Path ? (int)std::min<int64_t>(M, v.nt / v.P) : 1;
+        for (int U = 1; U <= umax; ++U) {
+            int occ = 0;
+            if (v.occupancy(U, &occ) != cudaSuccess || occ < 1) continue;
+            const double t = model_cycles(v, B, M, sms, U, occ, D);
+            if (t < best_t * 0.995) {
+                best_t = t;
+                best.v = &v;
+                best.U = U;
+            }
         }
     }
-    return bestu;
+    return best;
 }
 
 struct PlanKey {
-    const Variant* v;
-    int dev;
+    int d, N, dev;
+    bool f64;
     int64_t B, M;
-    bool operator==(const PlanKey& o) const { return v == o.v && dev == o.dev && B == o.B && M == o.M; }
+    bool operator==(const PlanKey& o) const {
+        return d == o.d && N == o.N && dev == o.dev && f64 == o.f64 && B == o.B && M == o.M;
+    }
 };
 
-static int cached_plan(const Variant& v, int dev, int64_t B, int64_t M) {
+static Plan cached_plan(int d, int N, bool is_f64, int dev, int64_t B, int64_t M, int64_t D) {
     static std::mutex mu;
-    static std::vector<std::pair<PlanKey, int>> cache;
-    const PlanKey key{&v, dev, B, M};
+    static std::vector<std::pair<PlanKey, Plan>> cache;
+    const PlanKey key{d, N, dev, is_f64, B, M};
     {
         std::lock_guard<std::mutex> g(mu);
         for (auto& kv : cache)
             if (kv.first == key) return kv.second;
     }
-    const int U = plan_units(v, B, M, device_info(dev).sms);
+    const Plan p = plan_launch(d, N, is_f64, B, M, device_info(dev).sms, D);
     std::lock_guard<std::mutex> g(mu);
     if (cache.size() > 256) cache.clear();
-    cache.emplace_back(key, U);
-    return U;
+    cache.emplace_back(key, p);
+    return p;
 }
 
 template <typename Real>
@@ -170,7 +207,18 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         if (cap == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
         else cudaEventRecord(ev, s);
     };
-    const Variant* v = (tun && tun->force_generic) ? nullptr : find_variant(d, N, is_f64);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int64_t plan_rows = (tun && tun->plan_rows > 0) ? tun->plan_rows : B;
+    Plan plan;
+    if (!(tun && tun->force_generic)) plan = cached_plan(d, N, is_f64, dev, plan_rows, M, D);
+    if (plan.v && tun && tun->prefix_len > 0) {  // pin Q (tests / tuning)
+        const Variant* cands[4];
+        const int nc = find_variants(d, N, is_f64, cands, 4);
+        for (int k = 0; k < nc; ++k)
+            if (cands[k]->Q == tun->prefix_len) plan.v = cands[k];
+    }
+    const Variant* v = plan.v;
     if (v == nullptr) {
         record(ev0);
         e = is_f64 ? launch_generic_f64(X, B, L, d, N, out, s) : launch_generic_f32(X, B, L, d, N, out, s);
@@ -184,18 +232,18 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         if (st) *st = local;
         return SIGK_OK;
     }
-    int dev = 0;
-    cudaGetDevice(&dev);
     int U = 1;
     if (v->family == KernelFamily::Path) {
-        const int64_t plan_rows = (tun && tun->plan_rows > 0) ? tun->plan_rows : B;
-        U = (tun && tun->chunks > 0) ? tun->chunks : cached_plan(*v, dev, plan_rows, M);
+        U = (tun && tun->chunks > 0) ? tun->chunks : plan.U;
         U = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)U, M, (int64_t)(v->nt / v->P)}));
         int occ = 0;
-        e = v->occupancy(U, &occ);
-        if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
-        if (occ < 1) return fail(SIGK_ERESOURCE, "fold variant does not fit on this device with " +
-                                                     std::to_string(U) + " chunks per path");
+        for (;;) {  // a forced chunk count may exceed the shared-memory budget: shrink it
+            e = v->occupancy(U, &occ);
+            if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+            if (occ >= 1 || U == 1) break;
+            --U;
+        }
+        if (occ < 1) return fail(SIGK_ERESOURCE, "fold variant does not fit on this device");
     }
     record(ev0);
     e = v->launch(X, B, L, U, out, s);

@@ -45,7 +45,8 @@ template <typename Real, int DIM, int DEPTH, int Q>
 struct PathVariant {
     using G = PathGeom<Real, DIM, DEPTH, Q>;
     using SF = typename G::SF;
-    static constexpr int NTMAX = 256;
+    // small slices leave room for 512-thread CTAs (<= 128 registers per thread)
+    static constexpr int NTMAX = (SF::S * (int)(sizeof(Real) / 4) <= 48 && SF::P <= 512) ? 512 : 256;
     static constexpr int T = G::tile_steps();
     static constexpr auto kernel = path_kernel<Real, DIM, DEPTH, Q, NTMAX, T>;
     static std::atomic<uint64_t> smem_done;
@@ -96,23 +97,35 @@ struct FlatVariant {
 template <typename Real, int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> FlatVariant<Real, DIM, DEPTH, Q>::smem_done{0};
 
+template <typename Real, int DIM, int DEPTH, int Q>
+Variant make_variant() {
+    using SF = SliceFold<Real, DIM, DEPTH, Q>;
+    int chen = 0;
+    for (int n = 2; n <= DEPTH; ++n) chen += (n - 1) * ipow(DIM, n);
+    const int loads = SF::VEC / SF::VW + Q * (SF::SCW / SF::VW);
+    if constexpr (SF::P > 256) {
+        using V = FlatVariant<Real, DIM, DEPTH, Q>;
+        return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Flat, V::NT, V::T,
+                       &V::launch, &V::occupancy};
+    } else {
+        using V = PathVariant<Real, DIM, DEPTH, Q>;
+        return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Path, V::NTMAX, V::T,
+                       &V::launch, &V::occupancy};
+    }
+}
+
+// Candidates per (precision, d, N): the smallest register-feasible prefix
+// length Q0 and, when it still fits a CTA, Q0 + 1 (more threads per unit, so
+// fewer sequence chunks and a cheaper merge tree at some redundant work). The
+// planner (sigk_abi.cu) picks per call from a cycle model.
 template <typename Real, int DIM, int DEPTH>
 struct VariantImpl {
-    static constexpr int Q = pick_q<Real>(DIM, DEPTH);
-    using SF = SliceFold<Real, DIM, DEPTH, Q>;
-    static constexpr bool FLAT = SF::P > 256;
-    static Variant make() {
-        int chen = 0;
-        for (int n = 2; n <= DEPTH; ++n) chen += (n - 1) * ipow(DIM, n);
-        if constexpr (FLAT) {
-            using V = FlatVariant<Real, DIM, DEPTH, Q>;
-            return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), chen, KernelFamily::Flat, V::NT, V::T,
-                           &V::launch, &V::occupancy};
-        } else {
-            using V = PathVariant<Real, DIM, DEPTH, Q>;
-            return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), chen, KernelFamily::Path, V::NTMAX, V::T,
-                           &V::launch, &V::occupancy};
-        }
+    static constexpr int Q0 = pick_q<Real>(DIM, DEPTH);
+    static constexpr bool SECOND = DIM > 1 && Q0 + 1 < DEPTH && ipow(DIM, Q0 + 1) <= 256 && ipow(DIM, Q0) <= 256;
+    static constexpr int count = SECOND ? 2 : 1;
+    static void fill(Variant* out) {
+        out[0] = make_variant<Real, DIM, DEPTH, Q0>();
+        if constexpr (SECOND) out[1] = make_variant<Real, DIM, DEPTH, Q0 + 1>();
     }
 };
 
@@ -121,11 +134,17 @@ void register_variants(const Variant* table, int n, bool is_f64);
 
 template <typename Real, int DIM, int... Ns>
 struct DimTable {
+    static constexpr int count = (VariantImpl<Real, DIM, Ns>::count + ...);
     static const Variant* table() {
-        static const Variant t[] = {VariantImpl<Real, DIM, Ns>::make()...};
+        static Variant t[count];
+        static bool done = false;
+        if (!done) {
+            int i = 0;
+            ((VariantImpl<Real, DIM, Ns>::fill(t + i), i += VariantImpl<Real, DIM, Ns>::count), ...);
+            done = true;
+        }
         return t;
     }
-    static constexpr int count = sizeof...(Ns);
 };
 
 }  // namespace sigk
