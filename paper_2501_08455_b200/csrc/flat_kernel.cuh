@@ -121,9 +121,7 @@ __global__ void __launch_bounds__(NT, MINB) flat_kernel(const Real* __restrict__
         store(buf);
         __syncthreads();
         if (tile + 1 < ntiles) load(tile + 1);
-        const Real* base = tab + (size_t)buf * T * NU * TAB + (size_t)uu * TAB;
-#pragma unroll 1
-        for (int s = 0; s < T; ++s) consume_step<SF>(st, base + (size_t)s * NU * TAB, dig);
+        consume_tile<SF, T>(st, tab + (size_t)buf * T * NU * TAB + (size_t)uu * TAB, (size_t)NU * TAB, dig);
     }
     __syncthreads();
     if (!active) {

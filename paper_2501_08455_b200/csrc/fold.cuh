@@ -174,23 +174,28 @@ __device__ __forceinline__ void store_slice(Real (&st)[SF::S], int pre, Real* __
     store_levels<SF, 1>(st, pre, row);
 }
 
-// Load the step's table row (δ/m vectors + the thread's prefix scalars) from
-// shared memory with 16-byte broadcast loads and apply one Horner step.
+// The operands of one Horner step, in registers: the δ/m vectors and the
+// thread's prefix scalars δ[p_k]/m.
 template <typename SF, typename Real>
-__device__ __forceinline__ void consume_step(Real (&st)[SF::S], const Real* __restrict__ row, const int (&dig)[SF::QS]) {
+struct StepRegs {
+    Real vs[SF::VEC];
+    Real sc[SF::QS][SF::SCW > 0 ? SF::SCW : 1];
+};
+
+// Load a step's table row from shared memory with 16-byte broadcast loads.
+template <typename SF, typename Real>
+__device__ __forceinline__ void load_row(StepRegs<SF, Real>& r, const Real* __restrict__ row, const int (&dig)[SF::QS]) {
     using V = typename Vec16<Real>::type;
     constexpr int VW = SF::VW, VEC = SF::VEC, SCW = SF::SCW;
-    Real vs[VEC];
 #pragma unroll
     for (int i = 0; i < VEC / VW; ++i) {
         const V v = reinterpret_cast<const V*>(row)[i];
         if constexpr (VW == 4) {
-            vs[4 * i] = v.x; vs[4 * i + 1] = v.y; vs[4 * i + 2] = v.z; vs[4 * i + 3] = v.w;
+            r.vs[4 * i] = v.x; r.vs[4 * i + 1] = v.y; r.vs[4 * i + 2] = v.z; r.vs[4 * i + 3] = v.w;
         } else {
-            vs[2 * i] = v.x; vs[2 * i + 1] = v.y;
+            r.vs[2 * i] = v.x; r.vs[2 * i + 1] = v.y;
         }
     }
-    Real sc[SF::QS][SCW > 0 ? SCW : 1];
     if constexpr (SF::QQ > 0) {
 #pragma unroll
         for (int k = 0; k < SF::QQ; ++k) {
@@ -199,16 +204,32 @@ __device__ __forceinline__ void consume_step(Real (&st)[SF::S], const Real* __re
             for (int i = 0; i < SCW / VW; ++i) {
                 const V v = reinterpret_cast<const V*>(sr)[i];
                 if constexpr (VW == 4) {
-                    sc[k][4 * i] = v.x; sc[k][4 * i + 1] = v.y; sc[k][4 * i + 2] = v.z; sc[k][4 * i + 3] = v.w;
+                    r.sc[k][4 * i] = v.x; r.sc[k][4 * i + 1] = v.y; r.sc[k][4 * i + 2] = v.z; r.sc[k][4 * i + 3] = v.w;
                 } else {
-                    sc[k][2 * i] = v.x; sc[k][2 * i + 1] = v.y;
+                    r.sc[k][2 * i] = v.x; r.sc[k][2 * i + 1] = v.y;
                 }
             }
         }
     } else {
-        sc[0][0] = Real(0);
+        r.sc[0][0] = Real(0);
     }
-    SF::step(st, vs, sc);
+}
+
+// The T steps of one tile (rows base, base + stride, ...), software-pipelined:
+// the row of step s+1 is in flight while the FFMAs of step s issue, so the
+// shared-memory latency never sits on the Horner chain.
+template <typename SF, int T, typename Real>
+__device__ __forceinline__ void consume_tile(Real (&st)[SF::S], const Real* __restrict__ base, size_t stride,
+                                             const int (&dig)[SF::QS]) {
+    StepRegs<SF, Real> ra, rb;
+    load_row<SF>(ra, base, dig);
+#pragma unroll 1
+    for (int s = 0; s < T; s += 2) {
+        if (s + 1 < T) load_row<SF>(rb, base + (size_t)(s + 1) * stride, dig);
+        SF::step(st, ra.vs, ra.sc);
+        if (s + 2 < T) load_row<SF>(ra, base + (size_t)(s + 2) * stride, dig);
+        if (s + 1 < T) SF::step(st, rb.vs, rb.sc);
+    }
 }
 
 // Write one increment δ (component c of step s) into a table row: the vector

@@ -42,8 +42,8 @@ struct PathGeom {
 };
 
 // X: (B, L, d); out: (B, D). grid = B, block = U * d^Q threads.
-template <typename Real, int DIM, int DEPTH, int Q, int NTMAX, int T>
-__global__ void __launch_bounds__(NTMAX) path_kernel(const Real* __restrict__ X, int64_t L, int U, int CL,
+template <typename Real, int DIM, int DEPTH, int Q, int NTMAX, int T, int MINB>
+__global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restrict__ X, int64_t L, int U, int CL,
                                                      Real* __restrict__ out) {
     using G = PathGeom<Real, DIM, DEPTH, Q>;
     using SF = typename G::SF;
@@ -75,6 +75,9 @@ __global__ void __launch_bounds__(NTMAX) path_kernel(const Real* __restrict__ X,
 
     constexpr int NX = G::nx(T);
     Real xr[NX];
+    // Q >= 2 producer geometry: thread tl handles channel c0 at steps s0, s0 + P/d, ...
+    const int s0 = tl / d, c0 = tl - (tl / d) * d;
+    const Real* __restrict__ xg = xu + (int64_t)s0 * d + c0;
     auto load = [&](int tile) {
         const int j0 = tile * T;
         if constexpr (RUN1) {  // channel c = tl, points j0 .. j0+T of the chunk
@@ -83,13 +86,12 @@ __global__ void __launch_bounds__(NTMAX) path_kernel(const Real* __restrict__ X,
         } else if constexpr (RUN0) {  // all channels, points j0 .. j0+T (contiguous)
 #pragma unroll
             for (int i = 0; i < (T + 1) * d; ++i) xr[i] = (j0 + i / d <= lim) ? __ldg(xu + (int64_t)j0 * d + i) : Real(0);
-        } else {
+        } else {  // entry i: step s0 + i*P/d of channel c0 (P is a multiple of d)
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
-                const int e = tl + i * P;
-                const int s = e / d, c = e - (e / d) * d;
-                const bool ok = (e < T * d) && (j0 + s < lim);
-                const Real* p = xu + (int64_t)(j0 + s) * d + c;
+                const int s = s0 + i * (P / d);
+                const bool ok = (s < T) && (j0 + s < lim);
+                const Real* p = xg + (int64_t)j0 * d + i * P;
                 xr[2 * i] = ok ? __ldg(p) : Real(0);
                 xr[2 * i + 1] = ok ? __ldg(p + d) : Real(0);
             }
@@ -114,11 +116,8 @@ __global__ void __launch_bounds__(NTMAX) path_kernel(const Real* __restrict__ X,
         } else {
 #pragma unroll
             for (int i = 0; i < EPT; ++i) {
-                const int e = tl + i * P;
-                if (e < T * d) {
-                    const int s = e / d, c = e - (e / d) * d;
-                    produce_entry<SF>(base + ((size_t)s * U + u) * TAB, c, xr[2 * i + 1] - xr[2 * i]);
-                }
+                const int s = s0 + i * (P / d);
+                if (s < T) produce_entry<SF>(base + (size_t)s * U * TAB + (size_t)u * TAB, c0, xr[2 * i + 1] - xr[2 * i]);
             }
         }
     };
@@ -130,9 +129,7 @@ __global__ void __launch_bounds__(NTMAX) path_kernel(const Real* __restrict__ X,
         store(buf, tile);
         __syncthreads();
         if (tile + 1 < ntiles) load(tile + 1);
-        const Real* base = tab + (size_t)buf * T * U * TAB + (size_t)u * TAB;
-#pragma unroll 1
-        for (int s = 0; s < T; ++s) consume_step<SF>(st, base + (size_t)s * U * TAB, dig);
+        consume_tile<SF, T>(st, tab + (size_t)buf * T * U * TAB + (size_t)u * TAB, (size_t)U * TAB, dig);
     }
 
     __syncthreads();  // the table is dead; reuse it for the chunk signatures

@@ -45,10 +45,14 @@ template <typename Real, int DIM, int DEPTH, int Q>
 struct PathVariant {
     using G = PathGeom<Real, DIM, DEPTH, Q>;
     using SF = typename G::SF;
-    // small slices leave room for 512-thread CTAs (<= 128 registers per thread)
-    static constexpr int NTMAX = (SF::S * (int)(sizeof(Real) / 4) <= 48 && SF::P <= 512) ? 512 : 256;
+    // Register budget from the slice size: small slices get 512-thread CTAs, mid
+    // slices 256 threads at >= 2 CTAs/SM (both <= 128 registers per thread), big
+    // slices 256 threads with up to 255 registers.
+    static constexpr int S32 = SF::S * (int)(sizeof(Real) / 4);
+    static constexpr int NTMAX = S32 <= 48 ? 512 : 256;
+    static constexpr int MINB = (S32 > 48 && S32 <= 96) ? 2 : 1;
     static constexpr int T = G::tile_steps();
-    static constexpr auto kernel = path_kernel<Real, DIM, DEPTH, Q, NTMAX, T>;
+    static constexpr auto kernel = path_kernel<Real, DIM, DEPTH, Q, NTMAX, T, MINB>;
     static std::atomic<uint64_t> smem_done;
 
     static cudaError_t launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s) {
