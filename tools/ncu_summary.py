@@ -51,3 +51,27 @@ for a, s, e, w in data:
 for a, s, e, n, w, ops in regions:
     if e * n > tot * 0.01 or w > totw * 0.02:
         print(f"{a[-5:]} exec={e:8d} n={n:4d} inst={e*n/tot:6.1%} stall={w/totw:6.1%} {dict(ops.most_common(6))}")
+
+# per-region stall breakdown
+sc = [i for i, x in enumerate(h) if x.startswith("stall_") and "Not Issued" not in x]
+reg_stalls = []
+cur = None
+for x in rows[2:]:
+    if len(x) < len(h):
+        continue
+    try:
+        e = int(x[ei] or 0)
+    except ValueError:
+        continue
+    if cur is None or cur[0] != e:
+        cur = [e, Counter(), x[ai]]
+        reg_stalls.append(cur)
+    for i in sc:
+        try:
+            cur[1][h[i]] += int(x[i] or 0)
+        except ValueError:
+            pass
+for e, c, a in reg_stalls:
+    t = sum(c.values())
+    if t > totw * 0.03:
+        print(f"{a[-5:]} stall={t/totw:5.1%} " + ", ".join(f"{k[6:]}={v/t:.0%}" for k, v in c.most_common(4)))

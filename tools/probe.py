@@ -13,6 +13,11 @@ cfg = {"c1": (32, 100, 2, 4), "c2": (128, 1000, 5, 4), "c3": (128, 10000, 5, 4),
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 Ks = sys.argv[2].split(",") if len(sys.argv) > 2 else ["0"]  # "K" or "K:Q"
 B, L, d, N = cfg[name]
+for a in sys.argv[3:]:
+    if a.startswith("B="):
+        B = int(a[2:])
+    if a.startswith("L="):
+        L = int(a[2:])
 X = torch.empty((B, L, d), device="cuda")
 sk.brownian(X)
 D = sk.sig_dim(d, N)
