@@ -83,6 +83,8 @@ typedef struct sigk_tuning {
     void* fold_event_stop;  /* ... and just after it */
     int32_t prefix_len;     /* pin Q, the leading indices owned per thread (0: planned) */
     int32_t reserved[3];
+    void* phase_buf;        /* optional device buffer of B*8 int64: per-CTA SM-clock
+                               timestamps of the path kernel's phases (profiling) */
 } sigk_tuning;
 
 int sigk_sig_dim(int d, int N, size_t* D);

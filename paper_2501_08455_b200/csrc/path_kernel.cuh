@@ -44,7 +44,7 @@ struct PathGeom {
 // X: (B, L, d); out: (B, D). grid = B, block = U * d^Q threads.
 template <typename Real, int DIM, int DEPTH, int Q, int NTMAX, int T, int MINB>
 __global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restrict__ X, int64_t L, int U, int CL,
-                                                     Real* __restrict__ out) {
+                                                           Real* __restrict__ out, long long* __restrict__ phases) {
     using G = PathGeom<Real, DIM, DEPTH, Q>;
     using SF = typename G::SF;
     constexpr int d = DIM;
@@ -122,23 +122,33 @@ __global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restric
         }
     };
 
+    // optional phase timestamps (SM clock) of thread 0, for tools/probe.py
+    auto phase = [&](int k) {
+        if (phases != nullptr && tid == 0) phases[b * 8 + k] = clock64();
+    };
+    phase(0);
     const int ntiles = (CL + T - 1) / T;
     load(0);
     for (int tile = 0; tile < ntiles; ++tile) {
         const int buf = tile & 1;
         store(buf, tile);
         __syncthreads();
+        if (tile == 0) phase(1);
         if (tile + 1 < ntiles) load(tile + 1);
         consume_tile<SF, T>(st, tab + (size_t)buf * T * U * TAB + (size_t)u * TAB, (size_t)U * TAB, dig);
     }
-
+    phase(2);
     __syncthreads();  // the table is dead; reuse it for the chunk signatures
+    phase(3);
     Real* sig = tab;
     store_slice<SF>(st, tl, sig + (size_t)u * D);
     __syncthreads();
+    phase(4);
     if (U > 1) merge_tree_smem<Real, d, DEPTH>(sig, U);
+    phase(5);
     Real* ob = out + b * D;
     for (int i = tid; i < D; i += blockDim.x) ob[i] = sig[i];
+    phase(6);
 }
 
 }  // namespace sigk

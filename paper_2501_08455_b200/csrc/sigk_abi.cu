@@ -246,7 +246,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         if (occ < 1) return fail(SIGK_ERESOURCE, "fold variant does not fit on this device");
     }
     record(ev0);
-    e = v->launch(X, B, L, U, out, s);
+    e = v->launch(X, B, L, U, out, s, tun ? tun->phase_buf : nullptr);
     record(ev1);
     if (e != cudaSuccess) return cuda_fail(e, "fold launch");
     const int64_t CL = (M + U - 1) / U;

@@ -55,13 +55,14 @@ struct PathVariant {
     static constexpr auto kernel = path_kernel<Real, DIM, DEPTH, Q, NTMAX, T, MINB>;
     static std::atomic<uint64_t> smem_done;
 
-    static cudaError_t launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s) {
+    static cudaError_t launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, void* phases) {
         const int64_t M = L - 1;
         const int CL = (int)((M + U - 1) / U);
         const size_t smem = G::smem_bytes(T, U);
         cudaError_t e = opt_in_smem(kernel, smem, smem_done);
         if (e != cudaSuccess) return e;
-        kernel<<<(unsigned)B, U * SF::P, smem, s>>>(static_cast<const Real*>(X), L, U, CL, static_cast<Real*>(out));
+        kernel<<<(unsigned)B, U * SF::P, smem, s>>>(static_cast<const Real*>(X), L, U, CL, static_cast<Real*>(out),
+                                                    static_cast<long long*>(phases));
         return cudaGetLastError();
     }
     static cudaError_t occupancy(int U, int* blocks) {
@@ -84,7 +85,7 @@ struct FlatVariant {
     static constexpr auto kernel = flat_kernel<Real, DIM, DEPTH, Q, NT, T, MINB>;
     static std::atomic<uint64_t> smem_done;
 
-    static cudaError_t launch(const void* X, int64_t B, int64_t L, int, void* out, cudaStream_t s) {
+    static cudaError_t launch(const void* X, int64_t B, int64_t L, int, void* out, cudaStream_t s, void*) {
         cudaError_t e = opt_in_smem(kernel, G::smem, smem_done);
         if (e != cudaSuccess) return e;
         const int64_t lanes = B * (int64_t)SF::P;
