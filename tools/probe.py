@@ -1,4 +1,8 @@
-"""Quick device-side probes: fold/merge event timings for a config across chunk counts."""
+"""Device-side probes: kernel event timings (and per-CTA phase clocks) for a
+config across (chunks, prefix length) choices.
+
+    python tools/probe.py c2 16:2,51:1 [B=1] [L=2] [phases]
+"""
 import ctypes as C
 import json
 import sys
@@ -13,34 +17,43 @@ cfg = {"c1": (32, 100, 2, 4), "c2": (128, 1000, 5, 4), "c3": (128, 10000, 5, 4),
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 Ks = sys.argv[2].split(",") if len(sys.argv) > 2 else ["0"]  # "K" or "K:Q"
 B, L, d, N = cfg[name]
+want_phases = False
 for a in sys.argv[3:]:
     if a.startswith("B="):
         B = int(a[2:])
-    if a.startswith("L="):
+    elif a.startswith("L="):
         L = int(a[2:])
+    elif a == "phases":
+        want_phases = True
 X = torch.empty((B, L, d), device="cuda")
 sk.brownian(X)
 D = sk.sig_dim(d, N)
 out = torch.empty((B, D), device="cuda")
+ph = torch.zeros((B, 8), dtype=torch.int64, device="cuda")
 s = torch.cuda.current_stream()
 for KQ in Ks:
     K, Qp = (int(x) for x in (KQ.split(":") + ["0"])[:2])
     res = []
     for it in range(6):
-        e0, e1, e2, e3 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        e0.record(); e1.record(); e3.record()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        e1.record()
         torch.cuda.synchronize()
         tun = sk._Tuning(chunks=K, prefix_len=Qp)
         tun.fold_event_start = C.c_void_p(e0.cuda_event)
         tun.fold_event_stop = C.c_void_p(e1.cuda_event)
+        if want_phases:
+            tun.phase_buf = C.c_void_p(ph.data_ptr())
         st = sk._Stats()
-        e2.record()
         sk._check(sk.lib().sigk_signature_f32(X.data_ptr(), B, L, d, N, out.data_ptr(), 3, C.c_void_p(s.cuda_stream),
                                               C.byref(tun), C.byref(st)))
-        e3.record()
         torch.cuda.synchronize()
-        res.append((e0.elapsed_time(e1) * 1e3, e2.elapsed_time(e3) * 1e3))
-    fold = min(r[0] for r in res)
-    tot = min(r[1] for r in res)
-    print(json.dumps({"cfg": name, "K": st.chunks, "Q": st.prefix_len, "CL": st.fold_steps, "fold_us": round(fold, 2),
-                      "total_us": round(tot, 2), "merge_us": round(tot - fold, 2)}))
+        res.append(e0.elapsed_time(e1) * 1e3)
+    rec = {"cfg": name, "B": B, "L": L, "K": st.chunks, "Q": st.prefix_len, "CL": st.fold_steps,
+           "kernel_us": round(min(res), 2)}
+    if want_phases:
+        p = ph.cpu()
+        dlt = (p[:, 1:7] - p[:, 0:6]).double().median(dim=0).values.tolist()
+        rec["phase_cycles"] = dict(zip(["first_tile", "fold", "sync", "stage", "merge", "write"], [int(x) for x in dlt]))
+        rec["total_cycles"] = int((p[:, 6] - p[:, 0]).double().median().item())
+    print(json.dumps(rec), flush=True)
