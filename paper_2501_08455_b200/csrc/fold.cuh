@@ -150,11 +150,12 @@ struct SliceFold {
     }
 };
 
-// Register state of one thread -> its slice of a flat (D) signature row.
-template <typename SF, int n, typename Real>
+// Register state of one thread -> its slice of degrees n..NMAX of a flat
+// signature row (degree m at offset level_off(d, m-1)).
+template <typename SF, int n, int NMAX, typename Real>
 __device__ __forceinline__ void store_levels(Real (&st)[SF::S], int pre, Real* __restrict__ row) {
     constexpr int d = SF::d, Q = SF::QQ;
-    if constexpr (n <= SF::N) {
+    if constexpr (n <= NMAX) {
         if constexpr (n >= SF::NMIN) {
             constexpr int sz = ipow(d, n - Q);
             constexpr int o = SF::top_off(n);
@@ -165,13 +166,19 @@ __device__ __forceinline__ void store_levels(Real (&st)[SF::S], int pre, Real* _
             constexpr int tail = ipow(d, Q - n);
             if (pre % tail == 0) row[level_off(d, n - 1) + pre / tail] = st[n - 1];
         }
-        store_levels<SF, n + 1>(st, pre, row);
+        store_levels<SF, n + 1, NMAX>(st, pre, row);
     }
 }
 
 template <typename SF, typename Real>
 __device__ __forceinline__ void store_slice(Real (&st)[SF::S], int pre, Real* __restrict__ row) {
-    store_levels<SF, 1>(st, pre, row);
+    store_levels<SF, 1, SF::N>(st, pre, row);
+}
+
+// Degrees 1..N-1 only (the inputs of the chunk combine, merge.cuh).
+template <typename SF, int n, typename Real>
+__device__ __forceinline__ void store_levels_below(Real (&st)[SF::S], int pre, Real* __restrict__ row) {
+    store_levels<SF, n, SF::N - 1>(st, pre, row);
 }
 
 // The operands of one Horner step, in registers: the δ/m vectors and the

@@ -1,70 +1,137 @@
-// Cross-chunk combine: Chen's identity as a fixed-order tree in shared memory.
+// Cross-chunk combine: the paper's per-degree cumulative-sum formulation
+// (arXiv 2501.08455 §2.2; reference parallel_forward, sig_core.hpp:175-298)
+// applied at CHUNK granularity, with Chen's identity (tensor_algebra.cpp:80-102)
+// giving each chunk's contribution.
 //
-// (A ⊠ B)_n = A_n + B_n + Σ_{i=1}^{n-1} A_i ⊗ B_{n-i}
-// (reference chen_product, /root/reference/proj/src/tensor_algebra.cpp:80-102,
-// same term order: c_n = a_n + b_n, then += a_i ⊗ b_{n-i} for i = 1..n-1).
+// Let C^(j) be the local signature of chunk j (folded from the identity) and
+// P^(j) = C^(0) ⊠ ... ⊠ C^(j-1) the exclusive prefix (P^(0) = 1). Then
+//     (P^(j) ⊠ C^(j))_n = P^(j)_n + c^(j)_n,
+//     c^(j)_n = C^(j)_n + Σ_{a=1}^{n-1} P^(j)_a ⊗ C^(j)_{n-a},
+// so P^(j)_n = Σ_{i<j} c^(i)_n is an exclusive prefix SUM over chunks of
+// contributions that need only the prefixes of LOWER degrees. Degree by
+// degree (n = 1..N-1): all chunks' contributions in parallel, then a plain
+// exclusive scan over chunks; the path's degree-n value is the scan total.
+// Degree N needs no scan, only the total Σ_j c^(j)_N — its cross terms are
+// formed in registers by the threads that already hold C^(j)_N's slices, and
+// the U contributions are summed in a fixed order (deterministic).
 //
-// The U chunk signatures of one path sit in shared memory (sig[u][D]). They
-// are combined pairwise in rounds h = 1, 2, 4, ...: slot j ← slot j ⊠ slot j+h
-// for j ≡ 0 (mod 2h). The order is fixed, so the result is deterministic and
-// independent of the launch shape. Each product overwrites its left operand
-// one level at a time in DESCENDING order with a CTA barrier between levels:
-// level n reads only levels < n of A, which are still intact. Inside a level
-// the work is split into runs of d consecutive outputs I = R*d + c (last index
-// varying): the whole run shares every prefix A_i[R / d^(n-i-1)] (one load
-// each) and reads contiguous suffix runs B_{n-i}[(R mod d^(n-i-1))*d + c], so
-// a run costs (n+1)d + n-1 loads for (n-1)d FMAs; all threads of the CTA share
-// the runs of every pair of the round. Divisors are compile-time.
+// Versus a log2(U)-round tree of full Chen products this has N phases, no
+// full products, and the dominant degree-N work runs FFMA-dense from
+// registers.
 #pragma once
 
-#include "sigk_common.cuh"
+#include "fold.cuh"
 
 namespace sigk {
 
-template <typename Real, int d, int n, int i>
-__device__ __forceinline__ void chen_run_terms(const Real* __restrict__ A, const Real* __restrict__ Bm, int R,
-                                               Real (&acc)[d]) {
-    if constexpr (i < n) {
-        constexpr int tail = ipow(d, n - i - 1);  // I / d^(n-i) = R / tail
-        const Real a = A[level_off(d, i - 1) + R / tail];
-        const Real* __restrict__ br = Bm + level_off(d, n - i - 1) + (R % tail) * d;
-#pragma unroll
-        for (int c = 0; c < d; ++c) acc[c] = fma(a, br[c], acc[c]);
-        chen_run_terms<Real, d, n, i + 1>(A, Bm, R, acc);
-    }
-}
-
+// Element-parallel contributions of degree n (< N) for all chunks, written in
+// place into pf's degree-n block, then the exclusive scan over chunks; the
+// scan totals (the path's degree-n coefficients) go to out.
 template <typename Real, int d, int N, int n>
-__device__ __forceinline__ void merge_level_desc(Real* __restrict__ sig, int D, int h, int pairs) {
-    if constexpr (n >= 1) {
-        constexpr int runs = ipow(d, n - 1);
+__device__ __forceinline__ void scan_lower_levels(const Real* __restrict__ cl, Real* __restrict__ pf, int U,
+                                                  Real* __restrict__ out) {
+    if constexpr (n < N) {
+        constexpr int DL = level_off(d, N - 1);
+        constexpr int lsz = ipow(d, n);
         constexpr int o = level_off(d, n - 1);
-        const int work = pairs * runs;
-        for (int w = threadIdx.x; w < work; w += blockDim.x) {
-            const int pj = w / runs;
-            const int R = w - pj * runs;
-            Real* A = sig + (2 * h * pj) * D;
-            const Real* Bm = A + h * D;
-            Real acc[d];
+        for (int w = threadIdx.x; w < U * lsz; w += blockDim.x) {
+            const int u = w / lsz, I = w - (w / lsz) * lsz;
+            const Real* c = cl + u * DL;
+            const Real* p = pf + u * DL;
+            Real acc = c[o + I];
 #pragma unroll
-            for (int c = 0; c < d; ++c) acc[c] = A[o + R * d + c] + Bm[o + R * d + c];
-            chen_run_terms<Real, d, n, 1>(A, Bm, R, acc);
-#pragma unroll
-            for (int c = 0; c < d; ++c) A[o + R * d + c] = acc[c];
+            for (int a = 1; a < n; ++a) {
+                const int tail = ipow(d, n - a);
+                acc = fma(p[level_off(d, a - 1) + I / tail], c[level_off(d, n - a - 1) + I % tail], acc);
+            }
+            pf[u * DL + o + I] = acc;
         }
         __syncthreads();
-        merge_level_desc<Real, d, N, n - 1>(sig, D, h, pairs);
+        for (int I = threadIdx.x; I < lsz; I += blockDim.x) {
+            Real acc = Real(0);
+            for (int u = 0; u < U; ++u) {
+                Real* q = pf + u * DL + o + I;
+                const Real t = *q;
+                *q = acc;
+                acc += t;
+            }
+            out[o + I] = acc;
+        }
+        __syncthreads();
+        scan_lower_levels<Real, d, N, n + 1>(cl, pf, U, out);
     }
 }
 
-// Tree-combine U signatures sig[0..U) (each D = level_off(d, N) values) into sig[0].
-// Must be called by every thread of the CTA (contains barriers).
-template <typename Real, int d, int N>
-__device__ __forceinline__ void merge_tree_smem(Real* __restrict__ sig, int U) {
-    constexpr int D = level_off(d, N);
-    for (int h = 1; h < U; h <<= 1) {
-        const int pairs = (U - h + 2 * h - 1) / (2 * h);  // j = 0, 2h, 4h, ... with j + h < U
-        merge_level_desc<Real, d, N, N>(sig, D, h, pairs);
+// Degree-N contribution of this thread's slice: st's top block plus
+// Σ_a P_a[(pre,J)[:a]] · C_{N-a}[(pre,J)[a:]] with P from pf and C's lower
+// degrees from cl (this chunk's rows). Accumulated into red (d^{N-Q} values).
+template <typename SF, int a, typename Real>
+__device__ __forceinline__ void top_cross_terms(const Real* __restrict__ p, const Real* __restrict__ c, int pre,
+                                                Real (&acc)[ipow(SF::d, SF::N - SF::QQ)]) {
+    constexpr int d = SF::d, N = SF::N, Q = SF::QQ;
+    if constexpr (a < N) {
+        constexpr int FJ = ipow(d, N - Q);  // outputs per thread
+        constexpr int tail = ipow(d, N - a);
+        const Real* pa = p + level_off(d, a - 1);
+        const Real* cb = c + level_off(d, N - a - 1);
+        if constexpr (a <= Q) {  // prefix scalar P_a[p_1..p_a]; suffix row C_{N-a}[(p_{a+1}..p_Q), J]
+            const Real pv = pa[pre / ipow(d, Q - a)];
+            const Real* cr = cb + (pre % ipow(d, Q - a)) * FJ;
+#pragma unroll
+            for (int J = 0; J < FJ; ++J) acc[J] = fma(pv, cr[J], acc[J]);
+        } else {  // prefix P_a[pre, J[:a-Q]] (slice of P), suffix C_{N-a}[J[a-Q:]]
+            const Real* pr = pa + pre * ipow(d, a - Q);
+#pragma unroll
+            for (int J = 0; J < FJ; ++J) acc[J] = fma(pr[J / tail], cb[J % tail], acc[J]);
+        }
+        top_cross_terms<SF, a + 1>(p, c, pre, acc);
+    }
+}
+
+// Per-thread stride of the degree-N contribution rows, padded when it is a
+// multiple of the 32 banks so the row stores do not conflict.
+template <typename SF>
+__host__ __device__ constexpr int red_stride() {
+    constexpr int FJ = ipow(SF::d, SF::N - SF::QQ);
+    return FJ % 32 == 0 ? FJ + 1 : FJ;
+}
+
+template <typename SF>
+__host__ __device__ constexpr size_t combine_smem_elems(int U) {
+    return (size_t)U * (2 * level_off(SF::d, SF::N - 1) + SF::P * red_stride<SF>());
+}
+
+// Combine the U chunk signatures held in registers by the CTA (thread (u, pre)
+// holds st = slice pre of chunk u) into the path's signature row `out`.
+// smem: at least U*(2*level_off(d,N-1) + d^N) Reals. Call from all threads.
+template <typename SF, typename Real>
+__device__ __forceinline__ void combine_chunks(Real (&st)[SF::S], int u, int pre, int U, Real* __restrict__ smem,
+                                               Real* __restrict__ out) {
+    constexpr int d = SF::d, N = SF::N, Q = SF::QQ;
+    constexpr int DL = level_off(d, N - 1);
+    constexpr int FJ = ipow(d, N - Q);
+    constexpr int FP = red_stride<SF>();  // padded per-thread stride: no bank conflicts
+    constexpr int o = level_off(d, N - 1);
+    Real* cl = smem;               // [U][DL] chunk signatures, degrees < N
+    Real* pf = cl + U * DL;        // [U][DL] exclusive prefixes
+    Real* red = pf + U * DL;       // [U][P][FP] degree-N contributions
+    store_levels_below<SF, 1>(st, pre, cl + u * DL);
+    __syncthreads();
+    scan_lower_levels<Real, d, N, 1>(cl, pf, U, out);
+    Real acc[FJ];
+#pragma unroll
+    for (int J = 0; J < FJ; ++J) acc[J] = st[SF::top_off(N) + J];
+    top_cross_terms<SF, 1>(pf + u * DL, cl + u * DL, pre, acc);
+    Real* r = red + (u * SF::P + pre) * FP;
+#pragma unroll
+    for (int J = 0; J < FJ; ++J) r[J] = acc[J];
+    __syncthreads();
+    constexpr int LN = ipow(d, N);
+    for (int F = threadIdx.x; F < LN; F += blockDim.x) {
+        const Real* q = red + (F / FJ) * FP + F % FJ;
+        Real s = Real(0);
+        for (int v = 0; v < U; ++v) s += q[v * SF::P * FP];
+        out[o + F] = s;
     }
 }
 

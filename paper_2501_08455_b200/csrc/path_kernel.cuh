@@ -36,8 +36,8 @@ struct PathGeom {
         return t < 1 ? 1 : (t > 8 ? 8 : t);
     }
     __host__ static size_t smem_bytes(int T, int U) {
-        const size_t tab = 2ull * T * U * SF::TAB, sig = (size_t)U * D;
-        return sizeof(Real) * (tab > sig ? tab : sig);
+        const size_t tab = 2ull * T * U * SF::TAB, comb = combine_smem_elems<SF>(U);
+        return sizeof(Real) * (tab > comb ? tab : comb);
     }
 };
 
@@ -138,17 +138,10 @@ __global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restric
         consume_tile<SF, T>(st, tab + (size_t)buf * T * U * TAB + (size_t)u * TAB, (size_t)U * TAB, dig);
     }
     phase(2);
-    __syncthreads();  // the table is dead; reuse it for the chunk signatures
+    __syncthreads();  // the table is dead; reuse it for the chunk combine
     phase(3);
-    Real* sig = tab;
-    store_slice<SF>(st, tl, sig + (size_t)u * D);
-    __syncthreads();
+    combine_chunks<SF>(st, u, tl, U, tab, out + b * D);
     phase(4);
-    if (U > 1) merge_tree_smem<Real, d, DEPTH>(sig, U);
-    phase(5);
-    Real* ob = out + b * D;
-    for (int i = tid; i < D; i += blockDim.x) ob[i] = sig[i];
-    phase(6);
 }
 
 }  // namespace sigk
