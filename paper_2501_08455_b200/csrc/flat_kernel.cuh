@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(NT, MINB) flat_kernel(const Real* __restrict__
         store(buf);
         __syncthreads();
         if (tile + 1 < ntiles) load(tile + 1);
-        consume_tile<SF, T>(st, tab + (size_t)buf * T * NU * TAB + (size_t)uu * TAB, (size_t)NU * TAB, dig);
+        consume_tile<SF, T, false>(st, tab + (size_t)buf * T * NU * TAB + (size_t)uu * TAB, (size_t)NU * TAB, dig);
     }
     __syncthreads();
     if (!active) {

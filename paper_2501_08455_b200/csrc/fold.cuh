@@ -225,9 +225,20 @@ __device__ __forceinline__ void load_row(StepRegs<SF, Real>& r, const Real* __re
 // The T steps of one tile (rows base, base + stride, ...), software-pipelined:
 // the row of step s+1 is in flight while the FFMAs of step s issue, so the
 // shared-memory latency never sits on the Horner chain.
-template <typename SF, int T, typename Real>
+// (PIPE = false: plain loop, for register-tight variants that hide the
+// latency with more resident warps instead.)
+template <typename SF, int T, bool PIPE = true, typename Real>
 __device__ __forceinline__ void consume_tile(Real (&st)[SF::S], const Real* __restrict__ base, size_t stride,
                                              const int (&dig)[SF::QS]) {
+    if constexpr (!PIPE) {
+#pragma unroll 1
+        for (int s = 0; s < T; ++s) {
+            StepRegs<SF, Real> r;
+            load_row<SF>(r, base + (size_t)s * stride, dig);
+            SF::step(st, r.vs, r.sc);
+        }
+        return;
+    }
     StepRegs<SF, Real> ra, rb;
     load_row<SF>(ra, base, dig);
 #pragma unroll 1

@@ -48,12 +48,17 @@ __device__ __forceinline__ void scan_lower_levels(const Real* __restrict__ cl, R
         }
         __syncthreads();
         for (int I = threadIdx.x; I < lsz; I += blockDim.x) {
+            Real* q = pf + o + I;
             Real acc = Real(0);
-            for (int u = 0; u < U; ++u) {
-                Real* q = pf + u * DL + o + I;
-                const Real t = *q;
-                *q = acc;
-                acc += t;
+            for (int u0 = 0; u0 < U; u0 += 8) {  // batches of 8 loads in flight
+                Real t[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) t[k] = (u0 + k < U) ? q[(u0 + k) * DL] : Real(0);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (u0 + k < U) q[(u0 + k) * DL] = acc;
+                    acc += t[k];
+                }
             }
             out[o + I] = acc;
         }
@@ -115,6 +120,16 @@ __device__ __forceinline__ void combine_chunks(Real (&st)[SF::S], int u, int pre
     Real* cl = smem;               // [U][DL] chunk signatures, degrees < N
     Real* pf = cl + U * DL;        // [U][DL] exclusive prefixes
     Real* red = pf + U * DL;       // [U][P][FP] degree-N contributions
+    if (U == 1) {  // a single chunk: its signature is the path's
+        store_levels_below<SF, 1>(st, pre, cl);
+        Real* r = red + pre * FP;
+#pragma unroll
+        for (int J = 0; J < FJ; ++J) r[J] = st[SF::top_off(N) + J];
+        __syncthreads();
+        for (int i = threadIdx.x; i < DL; i += blockDim.x) out[i] = cl[i];
+        for (int F = threadIdx.x; F < ipow(d, N); F += blockDim.x) out[o + F] = red[(F / FJ) * FP + F % FJ];
+        return;
+    }
     store_levels_below<SF, 1>(st, pre, cl + u * DL);
     __syncthreads();
     scan_lower_levels<Real, d, N, 1>(cl, pf, U, out);
@@ -130,7 +145,13 @@ __device__ __forceinline__ void combine_chunks(Real (&st)[SF::S], int u, int pre
     for (int F = threadIdx.x; F < LN; F += blockDim.x) {
         const Real* q = red + (F / FJ) * FP + F % FJ;
         Real s = Real(0);
-        for (int v = 0; v < U; ++v) s += q[v * SF::P * FP];
+        for (int v0 = 0; v0 < U; v0 += 8) {  // fixed summation order, 8 loads in flight
+            Real t[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t[k] = (v0 + k < U) ? q[(v0 + k) * SF::P * FP] : Real(0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += t[k];
+        }
         out[o + F] = s;
     }
 }

@@ -42,7 +42,7 @@ struct PathGeom {
 };
 
 // X: (B, L, d); out: (B, D). grid = B, block = U * d^Q threads.
-template <typename Real, int DIM, int DEPTH, int Q, int NTMAX, int T, int MINB>
+template <typename Real, int DIM, int DEPTH, int Q, int NTMAX, int T, int MINB, bool PIPE>
 __global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restrict__ X, int64_t L, int U, int CL,
                                                            Real* __restrict__ out, long long* __restrict__ phases) {
     using G = PathGeom<Real, DIM, DEPTH, Q>;
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restric
         __syncthreads();
         if (tile == 0) phase(1);
         if (tile + 1 < ntiles) load(tile + 1);
-        consume_tile<SF, T>(st, tab + (size_t)buf * T * U * TAB + (size_t)u * TAB, (size_t)U * TAB, dig);
+        consume_tile<SF, T, PIPE>(st, tab + (size_t)buf * T * U * TAB + (size_t)u * TAB, (size_t)U * TAB, dig);
     }
     phase(2);
     __syncthreads();  // the table is dead; reuse it for the chunk combine

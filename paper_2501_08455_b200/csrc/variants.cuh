@@ -52,7 +52,8 @@ struct PathVariant {
     static constexpr int NTMAX = S32 <= 48 ? 512 : 256;
     static constexpr int MINB = (S32 > 48 && S32 <= 96) ? 2 : 1;
     static constexpr int T = G::tile_steps();
-    static constexpr auto kernel = path_kernel<Real, DIM, DEPTH, Q, NTMAX, T, MINB>;
+    static constexpr bool PIPE = !(S32 > 48 && S32 <= 96);  // mid slices: more warps instead
+    static constexpr auto kernel = path_kernel<Real, DIM, DEPTH, Q, NTMAX, T, MINB, PIPE>;
     static std::atomic<uint64_t> smem_done;
 
     static cudaError_t launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, void* phases) {
