@@ -109,9 +109,9 @@ __host__ __device__ constexpr size_t combine_smem_elems(int U) {
 // Combine the U chunk signatures held in registers by the CTA (thread (u, pre)
 // holds st = slice pre of chunk u) into the path's signature row `out`.
 // smem: at least U*(2*level_off(d,N-1) + d^N) Reals. Call from all threads.
-template <typename SF, typename Real>
+template <typename SF, typename Real, typename Phase>
 __device__ __forceinline__ void combine_chunks(Real (&st)[SF::S], int u, int pre, int U, Real* __restrict__ smem,
-                                               Real* __restrict__ out) {
+                                               Real* __restrict__ out, Phase&& phase) {
     constexpr int d = SF::d, N = SF::N, Q = SF::QQ;
     constexpr int DL = level_off(d, N - 1);
     constexpr int FJ = ipow(d, N - Q);
@@ -132,7 +132,9 @@ __device__ __forceinline__ void combine_chunks(Real (&st)[SF::S], int u, int pre
     }
     store_levels_below<SF, 1>(st, pre, cl + u * DL);
     __syncthreads();
+    phase(4);
     scan_lower_levels<Real, d, N, 1>(cl, pf, U, out);
+    phase(5);
     Real acc[FJ];
 #pragma unroll
     for (int J = 0; J < FJ; ++J) acc[J] = st[SF::top_off(N) + J];
@@ -141,6 +143,7 @@ __device__ __forceinline__ void combine_chunks(Real (&st)[SF::S], int u, int pre
 #pragma unroll
     for (int J = 0; J < FJ; ++J) r[J] = acc[J];
     __syncthreads();
+    phase(6);
     constexpr int LN = ipow(d, N);
     for (int F = threadIdx.x; F < LN; F += blockDim.x) {
         const Real* q = red + (F / FJ) * FP + F % FJ;

@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restric
     phase(2);
     __syncthreads();  // the table is dead; reuse it for the chunk combine
     phase(3);
-    combine_chunks<SF>(st, u, tl, U, tab, out + b * D);
-    phase(4);
+    combine_chunks<SF>(st, u, tl, U, tab, out + b * D, phase);
+    phase(7);
 }
 
 }  // namespace sigk

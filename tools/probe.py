@@ -53,7 +53,12 @@ for KQ in Ks:
            "kernel_us": round(min(res), 2)}
     if want_phases:
         p = ph.cpu()
-        dlt = (p[:, 1:7] - p[:, 0:6]).double().median(dim=0).values.tolist()
-        rec["phase_cycles"] = dict(zip(["first_tile", "fold", "sync", "stage", "merge", "write"], [int(x) for x in dlt]))
-        rec["total_cycles"] = int((p[:, 6] - p[:, 0]).double().median().item())
+        names = ["first_tile", "fold", "sync", "store_lower", "scan_lower", "top_cross", "top_sum"]
+        if st.chunks == 1:  # U == 1 skips the scan phases
+            p[:, 6] = p[:, 3]
+            p[:, 4] = p[:, 3]
+            p[:, 5] = p[:, 3]
+        dlt = (p[:, 1:8] - p[:, 0:7]).double().median(dim=0).values.tolist()
+        rec["phase_cycles"] = dict(zip(names, [int(x) for x in dlt]))
+        rec["total_cycles"] = int((p[:, 7] - p[:, 0]).double().median().item())
     print(json.dumps(rec), flush=True)
