@@ -24,9 +24,11 @@
 
 namespace sigk {
 
-// Element-parallel contributions of degree n (< N) for all chunks, written in
-// place into pf's degree-n block, then the exclusive scan over chunks; the
-// scan totals (the path's degree-n coefficients) go to out.
+// Degree n (< N), fused: one thread per element I walks the chunks in order,
+// forming each chunk's contribution c_n[I] (from the already-scanned lower
+// prefixes) and writing the running exclusive sum into pf; the total (the
+// path's degree-n coefficient) goes to out. The walk is batched 8 chunks at a
+// time so the shared-memory loads of a batch are in flight together.
 template <typename Real, int d, int N, int n>
 __device__ __forceinline__ void scan_lower_levels(const Real* __restrict__ cl, Real* __restrict__ pf, int U,
                                                   Real* __restrict__ out) {
@@ -34,30 +36,34 @@ __device__ __forceinline__ void scan_lower_levels(const Real* __restrict__ cl, R
         constexpr int DL = level_off(d, N - 1);
         constexpr int lsz = ipow(d, n);
         constexpr int o = level_off(d, n - 1);
-        for (int w = threadIdx.x; w < U * lsz; w += blockDim.x) {
-            const int u = w / lsz, I = w - (w / lsz) * lsz;
-            const Real* c = cl + u * DL;
-            const Real* p = pf + u * DL;
-            Real acc = c[o + I];
+        for (int I = threadIdx.x; I < lsz; I += blockDim.x) {
+            // per-element offsets of the cross terms P_a[I / d^(n-a)] * C_{n-a}[I mod d^(n-a)]
+            int po[n > 1 ? n - 1 : 1], co[n > 1 ? n - 1 : 1];
 #pragma unroll
             for (int a = 1; a < n; ++a) {
                 const int tail = ipow(d, n - a);
-                acc = fma(p[level_off(d, a - 1) + I / tail], c[level_off(d, n - a - 1) + I % tail], acc);
+                po[a - 1] = level_off(d, a - 1) + I / tail;
+                co[a - 1] = level_off(d, n - a - 1) + I % tail;
             }
-            pf[u * DL + o + I] = acc;
-        }
-        __syncthreads();
-        for (int I = threadIdx.x; I < lsz; I += blockDim.x) {
-            Real* q = pf + o + I;
             Real acc = Real(0);
-            for (int u0 = 0; u0 < U; u0 += 8) {  // batches of 8 loads in flight
-                Real t[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) t[k] = (u0 + k < U) ? q[(u0 + k) * DL] : Real(0);
+            for (int u0 = 0; u0 < U; u0 += 8) {
+                Real c[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    if (u0 + k < U) q[(u0 + k) * DL] = acc;
-                    acc += t[k];
+                    const int u = u0 + k < U ? u0 + k : U - 1;
+                    const Real* cu = cl + u * DL;
+                    const Real* pu = pf + u * DL;
+                    Real x = cu[o + I];
+#pragma unroll
+                    for (int a = 1; a < n; ++a) x = fma(pu[po[a - 1]], cu[co[a - 1]], x);
+                    c[k] = x;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (u0 + k < U) {
+                        pf[(u0 + k) * DL + o + I] = acc;
+                        acc += c[k];
+                    }
                 }
             }
             out[o + I] = acc;
@@ -145,17 +151,30 @@ __device__ __forceinline__ void combine_chunks(Real (&st)[SF::S], int u, int pre
     __syncthreads();
     phase(6);
     constexpr int LN = ipow(d, N);
-    for (int F = threadIdx.x; F < LN; F += blockDim.x) {
-        const Real* q = red + (F / FJ) * FP + F % FJ;
-        Real s = Real(0);
-        for (int v0 = 0; v0 < U; v0 += 8) {  // fixed summation order, 8 loads in flight
-            Real t[8];
+    // fixed summation order over chunks; 2 elements x 8 chunks of loads in flight
+    for (int F0 = threadIdx.x; F0 < LN; F0 += 2 * blockDim.x) {
+        const int F1 = F0 + blockDim.x < LN ? F0 + blockDim.x : F0;
+        const Real* q0 = red + (F0 / FJ) * FP + F0 % FJ;
+        const Real* q1 = red + (F1 / FJ) * FP + F1 % FJ;
+        Real s0 = Real(0), s1 = Real(0);
+        for (int v0 = 0; v0 < U; v0 += 8) {
+            Real t0[8], t1[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) t[k] = (v0 + k < U) ? q[(v0 + k) * SF::P * FP] : Real(0);
+            for (int k = 0; k < 8; ++k) {
+                const int v = v0 + k < U ? v0 + k : U - 1;
+                t0[k] = q0[v * SF::P * FP];
+                t1[k] = q1[v * SF::P * FP];
+            }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) s += t[k];
+            for (int k = 0; k < 8; ++k) {
+                if (v0 + k < U) {
+                    s0 += t0[k];
+                    s1 += t1[k];
+                }
+            }
         }
-        out[o + F] = s;
+        out[o + F0] = s0;
+        if (F0 + blockDim.x < LN) out[o + F1] = s1;
     }
 }
 
