@@ -44,11 +44,18 @@ struct SliceFold {
         return o;
     }
     static constexpr int S = top_off(N + 1);         // registers of state per thread
-    static constexpr int NV = N - Q;                 // vector rows δ/m, m = 1..NV
+    // Operand modes. Table mode (Q <= 1): the table row holds every scaled
+    // vector δ/m (m = 1..N-Q) plus per-channel scalar rows δ[c]/m, so a step
+    // is pure FFMA. Lean mode (Q >= 2, where a thread's step is short and the
+    // shared-memory wavefronts per FFMA would bind): the row holds δ only; the
+    // thread reads δ[p_k] for its prefix digits and folds the 1/m factors into
+    // its (short) running products with a few FMULs.
+    static constexpr bool LEAN = Q >= 2;
+    static constexpr int NV = LEAN ? 1 : N - Q;      // vector rows δ/m, m = 1..NV
     static constexpr int VW = Vec16<Real>::n;
     static constexpr int VEC = round_up(NV * d, VW); // table: vector part
-    static constexpr int SCW = Q > 0 ? round_up(N, VW) : 0;
-    static constexpr int TAB = VEC + (Q > 0 ? d * SCW : 0);  // table row per (unit, step)
+    static constexpr int SCW = (Q > 0 && !LEAN) ? round_up(N, VW) : 0;
+    static constexpr int TAB = VEC + d * SCW;        // table row per (unit, step)
     static constexpr int QS = Q > 0 ? Q : 1;
     static constexpr int QQ = Q;
     // FFMA-pipe ops per thread per step (the Horner count restricted to a slice,
@@ -71,11 +78,14 @@ struct SliceFold {
         return k < Q ? st[k - 1] : st[top_off(Q)];
     }
 
-    // Level n of one Horner step. vs[(m-1)*d + c] = δ[c]/m ; sc[k-1][m-1] = δ[p_k]/m.
+    // Level n of one Horner step. Table mode: vs[(m-1)*d + c] = δ[c]/m,
+    // sc[k-1][m-1] = δ[p_k]/m. Lean mode: vs[c] = δ[c], sc[k-1][0] = δ[p_k].
     template <int n>
     __device__ __forceinline__ static void level(Real (&st)[S], const Real (&vs)[VEC],
                                                  const Real (&sc)[QS][SCW > 0 ? SCW : 1]) {
-        if constexpr (n > Q) {
+        if constexpr (LEAN) {
+            level_lean<n>(st, vs, sc);
+        } else if constexpr (n > Q) {
             constexpr int F = n - Q;  // free (per-thread) indices of level n
             Real u0 = Real(0);
             if constexpr (Q >= 1) {
@@ -119,6 +129,60 @@ struct SliceFold {
                 for (int k = 2; k <= n - 1; ++k) u = fma(u, sc[k - 1][n - k], scal(st, k));
                 scal(st, n) = fma(u, sc[n - 1][0], scal(st, n));
             }
+        }
+    }
+
+    // Lean-mode level n (Q >= 2): identical Horner chain, with δ/m formed as
+    // (running product * 1/m) * δ so only δ itself is read from the table.
+    template <int n>
+    __device__ __forceinline__ static void level_lean(Real (&st)[S], const Real (&dv)[VEC],
+                                                      const Real (&dp)[QS][SCW > 0 ? SCW : 1]) {
+        constexpr Real inv_n = Real(1) / Real(n);
+        if constexpr (n > Q) {
+            constexpr int F = n - Q;
+            Real u0 = fma(dp[0][0], inv_n, scal(st, 1));  // δ[p1]/n + T_1[p1]
+#pragma unroll
+            for (int k = 2; k <= Q; ++k) u0 = fma(u0 * (Real(1) / Real(n - k + 1)), dp[k - 1][0], scal(st, k));
+            if constexpr (F == 1) {
+                constexpr int o = top_off(n);
+#pragma unroll
+                for (int c = 0; c < d; ++c) st[o + c] = fma(u0, dv[c], st[o + c]);
+            } else {
+                Real ua[ipow(d, F - 1)];
+                {   // stage k = Q+1, factor 1/(n-Q)
+                    constexpr int o = top_off(Q + 1);
+                    const Real us = u0 * (Real(1) / Real(n - Q));
+#pragma unroll
+                    for (int c = 0; c < d; ++c) ua[c] = fma(us, dv[c], st[o + c]);
+                }
+                stages_lean<n, Q + 2>(st, dv, ua);
+                constexpr int o = top_off(n);
+#pragma unroll
+                for (int J = 0; J < ipow(d, F); ++J) st[o + J] = fma(ua[J / d], dv[J % d], st[o + J]);
+            }
+        } else {  // scalar level n <= Q
+            if constexpr (n == 1) {
+                scal(st, 1) += dp[0][0];
+            } else {
+                Real u = fma(dp[0][0], inv_n, scal(st, 1));
+#pragma unroll
+                for (int k = 2; k <= n - 1; ++k) u = fma(u * (Real(1) / Real(n - k + 1)), dp[k - 1][0], scal(st, k));
+                scal(st, n) = fma(u, dp[n - 1][0], scal(st, n));
+            }
+        }
+    }
+
+    template <int n, int k, int UA>
+    __device__ __forceinline__ static void stages_lean(Real (&st)[S], const Real (&dv)[VEC], Real (&ua)[UA]) {
+        if constexpr (k <= n - 1) {
+            constexpr int sz = ipow(d, k - Q);
+            constexpr int o = top_off(k);
+            constexpr Real inv = Real(1) / Real(n - k + 1);
+#pragma unroll
+            for (int J = 0; J < sz / d; ++J) ua[J] *= inv;  // prescale the previous stage
+#pragma unroll
+            for (int J = sz - 1; J >= 0; --J) ua[J] = fma(ua[J / d], dv[J % d], st[o + J]);
+            stages_lean<n, k + 1>(st, dv, ua);
         }
     }
 
@@ -203,7 +267,10 @@ __device__ __forceinline__ void load_row(StepRegs<SF, Real>& r, const Real* __re
             r.vs[2 * i] = v.x; r.vs[2 * i + 1] = v.y;
         }
     }
-    if constexpr (SF::QQ > 0) {
+    if constexpr (SF::LEAN) {  // δ[p_k]: one scalar load per prefix digit
+#pragma unroll
+        for (int k = 0; k < SF::QQ; ++k) r.sc[k][0] = row[dig[k]];
+    } else if constexpr (SF::QQ > 0) {
 #pragma unroll
         for (int k = 0; k < SF::QQ; ++k) {
             const Real* sr = row + VEC + dig[k] * SCW;
@@ -257,7 +324,7 @@ template <typename SF, typename Real>
 __device__ __forceinline__ void produce_entry(Real* __restrict__ row, int c, Real dl) {
 #pragma unroll
     for (int m = 1; m <= SF::NV; ++m) row[(m - 1) * SF::d + c] = dl * (Real(1) / Real(m));
-    if constexpr (SF::QQ > 0) {
+    if constexpr (SF::SCW > 0) {
 #pragma unroll
         for (int m = 1; m <= SF::N; ++m) row[SF::VEC + c * SF::SCW + (m - 1)] = dl * (Real(1) / Real(m));
     }
