@@ -46,25 +46,29 @@ __device__ __forceinline__ void scan_lower_levels(const Real* __restrict__ cl, R
                 co[a - 1] = level_off(d, n - a - 1) + I % tail;
             }
             Real acc = Real(0);
-            for (int u0 = 0; u0 < U; u0 += 8) {
+            const Real* cu = cl;
+            Real* pu = pf;
+            auto contrib = [&](const Real* c, const Real* p) {
+                Real x = c[o + I];
+#pragma unroll
+                for (int a = 1; a < n; ++a) x = fma(p[po[a - 1]], c[co[a - 1]], x);
+                return x;
+            };
+            int u = 0;
+            for (; u + 8 <= U; u += 8, cu += 8 * DL, pu += 8 * DL) {  // 8 chunks of loads in flight
                 Real c[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int u = u0 + k < U ? u0 + k : U - 1;
-                    const Real* cu = cl + u * DL;
-                    const Real* pu = pf + u * DL;
-                    Real x = cu[o + I];
-#pragma unroll
-                    for (int a = 1; a < n; ++a) x = fma(pu[po[a - 1]], cu[co[a - 1]], x);
-                    c[k] = x;
-                }
+                for (int k = 0; k < 8; ++k) c[k] = contrib(cu + k * DL, pu + k * DL);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    if (u0 + k < U) {
-                        pf[(u0 + k) * DL + o + I] = acc;
-                        acc += c[k];
-                    }
+                    pu[k * DL + o + I] = acc;
+                    acc += c[k];
                 }
+            }
+            for (; u < U; ++u, cu += DL, pu += DL) {
+                const Real x = contrib(cu, pu);
+                pu[o + I] = acc;
+                acc += x;
             }
             out[o + I] = acc;
         }
@@ -156,22 +160,25 @@ __device__ __forceinline__ void combine_chunks(Real (&st)[SF::S], int u, int pre
         const int F1 = F0 + blockDim.x < LN ? F0 + blockDim.x : F0;
         const Real* q0 = red + (F0 / FJ) * FP + F0 % FJ;
         const Real* q1 = red + (F1 / FJ) * FP + F1 % FJ;
+        constexpr int RS = SF::P * FP;  // stride between chunks
         Real s0 = Real(0), s1 = Real(0);
-        for (int v0 = 0; v0 < U; v0 += 8) {
+        int v = 0;
+        for (; v + 8 <= U; v += 8, q0 += 8 * RS, q1 += 8 * RS) {
             Real t0[8], t1[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                const int v = v0 + k < U ? v0 + k : U - 1;
-                t0[k] = q0[v * SF::P * FP];
-                t1[k] = q1[v * SF::P * FP];
+                t0[k] = q0[k * RS];
+                t1[k] = q1[k * RS];
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                if (v0 + k < U) {
-                    s0 += t0[k];
-                    s1 += t1[k];
-                }
+                s0 += t0[k];
+                s1 += t1[k];
             }
+        }
+        for (; v < U; ++v, q0 += RS, q1 += RS) {
+            s0 += *q0;
+            s1 += *q1;
         }
         out[o + F0] = s0;
         if (F0 + blockDim.x < LN) out[o + F1] = s1;
