@@ -82,7 +82,12 @@ typedef struct sigk_tuning {
                                before the fold kernel (instrumentation) */
     void* fold_event_stop;  /* ... and just after it */
     int32_t prefix_len;     /* pin Q, the leading indices owned per thread (0: planned) */
-    int32_t reserved[3];
+    int32_t no_overlap;     /* 1: never launch as a programmatic dependent launch. By
+                               default a fold kernel may start while the previous
+                               sigk kernel on the same stream finishes (its output
+                               writes still wait), unless X overlaps that kernel's
+                               output. */
+    int32_t reserved[2];
     void* phase_buf;        /* optional device buffer of B*8 int64: per-CTA SM-clock
                                timestamps of the path kernel's phases (profiling) */
 } sigk_tuning;

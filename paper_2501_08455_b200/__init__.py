@@ -49,7 +49,7 @@ class _Stats(C.Structure):
 class _Tuning(C.Structure):
     _fields_ = [("chunks", C.c_int32), ("force_generic", C.c_int32), ("plan_rows", C.c_int64),
                 ("fold_event_start", C.c_void_p), ("fold_event_stop", C.c_void_p), ("prefix_len", C.c_int32),
-                ("reserved", C.c_int32 * 3), ("phase_buf", C.c_void_p)]
+                ("no_overlap", C.c_int32), ("reserved", C.c_int32 * 2), ("phase_buf", C.c_void_p)]
 
 
 @dataclass

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(NT, MINB) flat_kernel(const Real* __restrict__
     Real st[SF::S];
 #pragma unroll
     for (int i = 0; i < SF::S; ++i) st[i] = Real(0);
+    pdl_trigger();
 
     // producer entries e = (unit ue, step s, channel c), c fastest: per-thread
     // offsets (from the CTA's first path, relative to the tile start) are fixed
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(NT, MINB) flat_kernel(const Real* __restrict__
         if (tile + 1 < ntiles) load(tile + 1);
         consume_tile<SF, T, false>(st, tab + (size_t)buf * T * NU * TAB + (size_t)uu * TAB, (size_t)NU * TAB, dig);
     }
+    pdl_wait();
     __syncthreads();
     if (!active) {
 #pragma unroll

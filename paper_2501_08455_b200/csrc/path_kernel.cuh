@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restric
         if (phases != nullptr && tid == 0) phases[b * 8 + k] = clock64();
     };
     phase(0);
+    pdl_trigger();  // the next launch may start folding on free SMs now
     const int ntiles = (CL + T - 1) / T;
     load(0);
     for (int tile = 0; tile < ntiles; ++tile) {
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(NTMAX, MINB) path_kernel(const Real* __restric
         consume_tile<SF, T, PIPE>(st, tab + (size_t)buf * T * U * TAB + (size_t)u * TAB, (size_t)U * TAB, dig);
     }
     phase(2);
+    pdl_wait();       // the previous launch has completed: our output writes are ordered after its
     __syncthreads();  // the table is dead; reuse it for the chunk combine
     phase(3);
     combine_chunks<SF>(st, u, tl, U, tab, out + b * D, phase);

@@ -174,6 +174,39 @@ static Plan cached_plan(int d, int N, bool is_f64, int dev, int64_t B, int64_t M
     return p;
 }
 
+// Programmatic-dependent-launch safety. A fold kernel launched with PDL may
+// start while the previous kernel on its stream still runs; it orders only
+// its OUTPUT writes after that kernel (griddepcontrol.wait), not its reads of
+// X. Only sigk's own fold kernels trigger dependents early, and they write
+// nothing but their output rows, so the overlap is safe unless X overlaps the
+// output of the previous sigk launch on the same stream (any other kernel in
+// between completes before ours can start). Remember each stream's last
+// output range and refuse the overlap when X intersects it.
+static bool may_overlap_previous(int dev, cudaStream_t s, const void* X, size_t xbytes, const void* out,
+                                 size_t obytes) {
+    struct Last {
+        int dev;
+        cudaStream_t s;
+        uintptr_t lo, hi;
+    };
+    static std::mutex mu;
+    static std::vector<Last> last;
+    const uintptr_t xlo = reinterpret_cast<uintptr_t>(X), xhi = xlo + xbytes;
+    const uintptr_t olo = reinterpret_cast<uintptr_t>(out), ohi = olo + obytes;
+    std::lock_guard<std::mutex> g(mu);
+    for (Last& l : last) {
+        if (l.dev == dev && l.s == s) {
+            const bool ok = xhi <= l.lo || xlo >= l.hi;
+            l.lo = olo;
+            l.hi = ohi;
+            return ok;
+        }
+    }
+    if (last.size() > 1024) last.clear();
+    last.push_back(Last{dev, s, olo, ohi});
+    return true;
+}
+
 template <typename Real>
 static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* out, cudaStream_t s,
                       const sigk_tuning* tun, sigk_stats* st) {
@@ -245,8 +278,10 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         }
         if (occ < 1) return fail(SIGK_ERESOURCE, "fold variant does not fit on this device");
     }
+    const bool overlap = !(tun && tun->no_overlap) &&
+                         may_overlap_previous(dev, s, X, sizeof(Real) * B * L * d, out, sizeof(Real) * B * D);
     record(ev0);
-    e = v->launch(X, B, L, U, out, s, tun ? tun->phase_buf : nullptr);
+    e = v->launch(X, B, L, U, out, s, tun ? tun->phase_buf : nullptr, overlap && !ev0);
     record(ev1);
     if (e != cudaSuccess) return cuda_fail(e, "fold launch");
     const int64_t CL = (M + U - 1) / U;

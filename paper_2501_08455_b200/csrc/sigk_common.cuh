@@ -28,6 +28,12 @@ __host__ __device__ constexpr int level_off(int d, int n) {  // start of degree 
     return o;
 }
 
+// Programmatic dependent launch (sm_90+): let the next kernel on the stream be
+// scheduled now / wait until the previous kernel on the stream has completed
+// and its memory is visible. Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Vector width (in elements) of one 16-byte shared-memory access.
 template <typename Real>
 struct Vec16;

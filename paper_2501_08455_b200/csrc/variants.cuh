@@ -41,6 +41,28 @@ cudaError_t opt_in_smem(K kern, size_t bytes, std::atomic<uint64_t>& done) {
     return e;
 }
 
+// Launch, optionally as a programmatic dependent launch (PDL): the grid may
+// start while the previous kernel on the stream is still running. The fold
+// kernels trigger their dependents at entry and execute griddepcontrol.wait
+// before their first global write, so only the output write is ordered after
+// the predecessor; the caller (sigk_abi.cu) enables this only when the input
+// cannot be the predecessor's output.
+template <typename K, typename... Args>
+cudaError_t launch_maybe_overlapped(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool overlap,
+                                    Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = overlap ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <typename Real, int DIM, int DEPTH, int Q>
 struct PathVariant {
     using G = PathGeom<Real, DIM, DEPTH, Q>;
@@ -56,15 +78,16 @@ struct PathVariant {
     static constexpr auto kernel = path_kernel<Real, DIM, DEPTH, Q, NTMAX, T, MINB, PIPE>;
     static std::atomic<uint64_t> smem_done;
 
-    static cudaError_t launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, void* phases) {
+    static cudaError_t launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, void* phases,
+                              bool overlap) {
         const int64_t M = L - 1;
         const int CL = (int)((M + U - 1) / U);
         const size_t smem = G::smem_bytes(T, U);
         cudaError_t e = opt_in_smem(kernel, smem, smem_done);
         if (e != cudaSuccess) return e;
-        kernel<<<(unsigned)B, U * SF::P, smem, s>>>(static_cast<const Real*>(X), L, U, CL, static_cast<Real*>(out),
-                                                    static_cast<long long*>(phases));
-        return cudaGetLastError();
+        return launch_maybe_overlapped(kernel, dim3((unsigned)B), dim3(U * SF::P), smem, s, overlap,
+                                       static_cast<const Real*>(X), L, U, CL, static_cast<Real*>(out),
+                                       static_cast<long long*>(phases));
     }
     static cudaError_t occupancy(int U, int* blocks) {
         const size_t smem = G::smem_bytes(T, U);
@@ -86,13 +109,13 @@ struct FlatVariant {
     static constexpr auto kernel = flat_kernel<Real, DIM, DEPTH, Q, NT, T, MINB>;
     static std::atomic<uint64_t> smem_done;
 
-    static cudaError_t launch(const void* X, int64_t B, int64_t L, int, void* out, cudaStream_t s, void*) {
+    static cudaError_t launch(const void* X, int64_t B, int64_t L, int, void* out, cudaStream_t s, void*,
+                              bool overlap) {
         cudaError_t e = opt_in_smem(kernel, G::smem, smem_done);
         if (e != cudaSuccess) return e;
         const int64_t lanes = B * (int64_t)SF::P;
-        kernel<<<(unsigned)((lanes + NT - 1) / NT), NT, G::smem, s>>>(static_cast<const Real*>(X), B, L,
-                                                                      static_cast<Real*>(out));
-        return cudaGetLastError();
+        return launch_maybe_overlapped(kernel, dim3((unsigned)((lanes + NT - 1) / NT)), dim3(NT), G::smem, s, overlap,
+                                       static_cast<const Real*>(X), B, L, static_cast<Real*>(out));
     }
     static cudaError_t occupancy(int, int* blocks) {
         cudaError_t e = opt_in_smem(kernel, G::smem, smem_done);

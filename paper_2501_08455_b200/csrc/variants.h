@@ -20,7 +20,8 @@ struct Variant {
     int nt;      // path: max threads per CTA; flat: threads per CTA
     int T;       // steps per shared-memory tile
     // path: grid = B CTAs of U*P threads (U chunks per path); flat: U ignored
-    cudaError_t (*launch)(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, void* phases);
+    cudaError_t (*launch)(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, void* phases,
+                          bool overlap_previous);
     // resident CTAs per SM for a given U (0 when it does not fit)
     cudaError_t (*occupancy)(int U, int* blocks_per_sm);
 };

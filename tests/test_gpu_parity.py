@@ -235,3 +235,35 @@ def test_sharded_entry_matches_single(sk):
     a = sk.signature(X, 4)
     b = sk.signature_sharded(X, 4, num_gpus=0)
     assert np.array_equal(a, b)
+
+
+def test_back_to_back_launches_overlap_safely(sk):
+    # consecutive calls on one stream may overlap (programmatic dependent launch);
+    # every result must still be exact and ordered
+    torch = pytest.importorskip("torch")
+    Xs = [torch.from_numpy(brownian(128, 1000, 5, seed=50 + i).astype(np.float32)).cuda() for i in range(6)]
+    outs = [torch.empty((128, 780), device="cuda") for _ in Xs]
+    shared = torch.empty((128, 780), device="cuda")
+    for X, o in zip(Xs, outs):
+        sk.signature(X, 4, out=o)
+        sk.signature(X, 4, out=shared)  # write-after-write on one buffer
+    torch.cuda.synchronize()
+    for X, o in zip(Xs, outs):
+        ref = O.signature(X.cpu().numpy().astype(np.float64), 4, threads=THREADS)
+        assert max(level_errors(o.cpu().numpy(), ref, 5, 4)) <= F32_TOL
+    assert torch.equal(shared, outs[-1])
+
+
+def test_input_produced_by_previous_call_is_serialised(sk):
+    # read-after-write through the library: the second call's paths ARE the first call's output
+    torch = pytest.importorskip("torch")
+    X1 = torch.from_numpy(brownian(64, 300, 3, seed=8).astype(np.float32)).cuda()
+    out1 = torch.empty((64, 39), device="cuda")  # d=3, N=3 -> D=39 = 13 points x 3 channels
+    for _ in range(3):
+        sk.signature(X1, 3, out=out1)
+        out2 = sk.signature(out1.view(64, 13, 3), 3)
+    torch.cuda.synchronize()
+    ref1 = O.signature(X1.cpu().numpy().astype(np.float64), 3, threads=THREADS)
+    X2 = out1.cpu().numpy().reshape(64, 13, 3).astype(np.float64)
+    assert max(level_errors(out1.cpu().numpy(), ref1, 3, 3)) <= F32_TOL
+    assert max(level_errors(out2.cpu().numpy(), O.signature(X2, 3), 3, 3)) <= F32_TOL
