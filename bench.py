@@ -43,6 +43,7 @@ CONFIGS = {
     "c5": (8192, 1000, 8, 4),
 }
 L2_BYTES = 126 * 1024 * 1024
+TUNE = {}  # sigk_tuning overrides from the command line (chunks / prefix_len)
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
@@ -289,7 +290,7 @@ def run_ours(args):
     Xh = pool[0].cpu().pin_memory()
     outh = torch.empty((B, D), dtype=torch.float32).pin_memory()
     lib = sk.lib()
-    tun = sk._Tuning()
+    tun = sk._Tuning(**TUNE)
     e2e_steps = max(3, min(args.steps, args.e2e_steps))
     for _ in range(3):
         sk._check(lib.sigk_signature_f32(Xh.data_ptr(), B, L, d, N, outh.data_ptr(), 0,
@@ -397,7 +398,7 @@ def _step(sk, X, N, out, ev):
 
     import torch
 
-    tun = sk._Tuning()
+    tun = sk._Tuning(**TUNE)
     if ev is not None:
         tun.fold_event_start = C.c_void_p(ev[0].cuda_event)
         tun.fold_event_stop = C.c_void_p(ev[1].cuda_event)
@@ -466,7 +467,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--chunks", type=int, default=0, help="force chunks per path (0: planned)")
+    ap.add_argument("--prefix-len", type=int, default=0, help="force Q (0: planned)")
     args = ap.parse_args()
+    TUNE.update(chunks=args.chunks, prefix_len=args.prefix_len)
     if args.impl == "reference":
         args.steps = args.steps or 5
         args.warmup = 1 if args.warmup is None else args.warmup
