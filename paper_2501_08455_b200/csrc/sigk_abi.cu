@@ -88,9 +88,11 @@ int find_variants(int d, int N, bool is_f64, const Variant** out, int max) {
 // Issue efficiency of the FFMA pipe vs resident warps per SM sub-partition
 // (measured on B200 with tools/ffma_probe.cu: ~0.62 at 1 warp, ~0.85 at 2).
 static double issue_eff(double warps_per_smsp) {
-    if (warps_per_smsp <= 1.0) return 0.62 * std::max(warps_per_smsp, 0.05);
-    if (warps_per_smsp <= 2.0) return 0.62 + 0.23 * (warps_per_smsp - 1.0);
-    return std::min(0.95, 0.85 + 0.05 * (warps_per_smsp - 2.0));
+    // saturates near 0.8: the fold's 3-register FFMAs dispatch at ~0.75/cycle/SMSP
+    // (tools/step_probe.cu), and the in-kernel loop adds shared-memory traffic
+    if (warps_per_smsp <= 1.0) return 0.55 * std::max(warps_per_smsp, 0.05);
+    if (warps_per_smsp <= 2.0) return 0.55 + 0.2 * (warps_per_smsp - 1.0);
+    return std::min(0.8, 0.75 + 0.05 * (warps_per_smsp - 2.0));
 }
 
 // Cycle model of one launch (SM cycles). Path kernel: a wave puts c CTAs of
@@ -116,7 +118,9 @@ static double model_cycles(const Variant& v, int64_t B, int64_t M, int sms, int 
     const double fold = c * threads * CL * per_step / 128.0 / eff;
     int rounds = 0;
     while ((1 << rounds) < U) ++rounds;
-    const double merge = c * (U - 1) * (double)D * 12.0 / 128.0 / eff + rounds * v.N * 120.0;
+    // combine (merge.cuh): ~20 issue slots per chunk per signature element, plus
+    // a barrier-bound latency per degree
+    const double merge = c * (U - 1) * (double)D * 20.0 / 128.0 / eff + rounds * v.N * 120.0;
     const double sync = (double)((CL + v.T - 1) / v.T) * 100.0;
     return waves * (fold + merge + sync);
 }
