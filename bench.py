@@ -208,7 +208,8 @@ def run_ours(args):
 
     st = sk.KernelStats()
     with torch.cuda.stream(stream):
-        sk.signature(pool[0], N, stats=st, out=out)
+        sk.signature(pool[0], N, stats=st, out=out, chunks=TUNE.get("chunks", 0),
+                     prefix_len=TUNE.get("prefix_len", 0))
     stream.synchronize()
 
     # FFMA-pipe peak on this GPU (roofline denominator)
