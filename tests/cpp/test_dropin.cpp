@@ -1,0 +1,147 @@
+// The reference's own kernel tests (proj/tests/test_kernels.cpp,
+// proj/tests/acceptance/acceptance.cpp), restated against the drop-in C++ API
+// (include/sigkit/*.hpp) backed by the B200 kernels. Built by
+// tests/test_cpp_dropin.py; exits non-zero on the first failure.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "sigkit/errors.hpp"
+#include "sigkit/kernels.hpp"
+#include "sigkit/tensor_algebra.hpp"
+
+using namespace sigkit;
+
+static int failures = 0;
+#define CHECK(cond)                                                          \
+    do {                                                                     \
+        if (!(cond)) {                                                       \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+            ++failures;                                                      \
+        }                                                                    \
+    } while (0)
+
+static PathBatch random_paths(unsigned seed, std::size_t B, std::size_t L, int d, double step) {
+    PathBatch p;
+    p.batch = B;
+    p.len = L;
+    p.dim = d;
+    p.values.assign(B * L * d, 0.0);
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> nd(0.0, 1.0);
+    for (std::size_t b = 0; b < B; ++b)
+        for (std::size_t t = 0; t < L; ++t)
+            for (int c = 0; c < d; ++c)
+                p.at(b, t, c) = (t ? p.at(b, t - 1, c) : 0.0) + step * nd(rng);
+    return p;
+}
+
+static double max_abs_diff(const std::vector<double>& a, const std::vector<double>& b) {
+    double m = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) m = std::fmax(m, std::fabs(a[i] - b[i]));
+    return m;
+}
+
+int main() {
+    // acceptance.cpp:54-58
+    CHECK(sig_dim(10, 4) == 11110 && sig_dim(2, 2) == 6 && sig_dim(6, 3) == 258);
+
+    // acceptance.cpp:195-209 — the corner path
+    {
+        PathBatch p;
+        p.batch = 1;
+        p.len = 3;
+        p.dim = 2;
+        p.values = {0, 0, 1, 0, 1, 1};
+        const std::vector<double> expected{1, 1, 0.5, 1, 0, 0.5};
+        for (KernelKind k : {KernelKind::Sequential, KernelKind::Parallel, KernelKind::Auto})
+            CHECK(max_abs_diff(signature(p, 2, k).flat, expected) < 1e-12);
+    }
+
+    // test_kernels.cpp:65-74 — a single point is the identity
+    {
+        const SignatureBatch s = signature(random_paths(21, 2, 1, 3, 1.0), 3);
+        CHECK(s.flat.size() == 2 * sig_dim(3, 3));
+        for (double x : s.flat) CHECK(x == 0.0);
+    }
+
+    // test_kernels.cpp:89-100 — two points give the restricted exponential
+    {
+        const PathBatch p = random_paths(23, 1, 2, 3, 1.0);
+        std::vector<double> v(3);
+        for (int c = 0; c < 3; ++c) v[c] = p.at(0, 1, c) - p.at(0, 0, c);
+        CHECK(max_abs_diff(signature_sequential(p, 4).flat, flatten(restricted_exp(v, 4)).coeffs) < 1e-14);
+    }
+
+    // test_kernels.cpp:148-171 — concatenation composes through the Chen product
+    for (unsigned seed = 40; seed < 45; ++seed) {
+        const PathBatch p = random_paths(seed, 1, 11, 3, 0.5);
+        PathBatch head, tail;
+        head.batch = tail.batch = 1;
+        head.dim = tail.dim = 3;
+        head.len = 5;
+        tail.len = 7;
+        head.values.assign(p.values.begin(), p.values.begin() + 15);
+        tail.values.assign(p.values.begin() + 12, p.values.end());
+        const FlatSignature a{3, 4, signature(head, 4).flat}, b{3, 4, signature(tail, 4).flat};
+        CHECK(max_abs_diff(signature(p, 4).flat, flatten(chen_product(unflatten(a), unflatten(b))).coeffs) < 1e-10);
+    }
+
+    // test_kernels.cpp:207-228 — scaling by lambda scales degree n by lambda^n
+    {
+        const PathBatch p = random_paths(100, 1, 6, 2, 1.0);
+        PathBatch s = p;
+        for (double& x : s.values) x *= 2.0;
+        const auto off = level_offsets(2, 4);
+        const SignatureBatch a = signature(p, 4), b = signature(s, 4);
+        double f = 1;
+        for (int n = 1; n <= 4; ++n) {
+            f *= 2.0;
+            for (std::size_t i = off[n - 1]; i < off[n]; ++i) CHECK(std::fabs(b.flat[i] - f * a.flat[i]) <= 1e-10 * (1 + std::fabs(f * a.flat[i])));
+        }
+    }
+
+    // test_kernels.cpp:119-126 and a long batch against the f32 entry
+    {
+        const SignatureBatch s = signature(random_paths(26, 1, 3, 10, 1.0), 4);
+        CHECK(s.width() == 11110);
+        const PathBatch p = random_paths(7, 32, 1000, 5, 1.0 / std::sqrt(999.0));
+        const SignatureBatch ref = signature(p, 4);
+        std::vector<float> x(p.values.begin(), p.values.end()), out(32 * 780);
+        KernelStats st;
+        signature_f32(x.data(), 32, 1000, 5, 4, out.data(), &st);
+        double scale = 0;
+        for (double v : ref.flat) scale = std::fmax(scale, std::fabs(v));
+        std::vector<double> o(out.begin(), out.end());
+        CHECK(max_abs_diff(o, ref.flat) <= 1e-5 * scale);
+        CHECK(st.fold_steps >= 1);
+    }
+
+    // test_kernels.cpp:334-346 — invalid shapes and depths, exception classes
+    {
+        PathBatch p;
+        p.batch = 1;
+        p.len = 3;
+        p.dim = 2;
+        p.values.assign(5, 0.0);
+        bool threw = false;
+        try { signature_sequential(p, 2); } catch (const DomainError&) { threw = true; }
+        CHECK(threw);
+        p.values.assign(6, 0.0);
+        threw = false;
+        try { signature(p, 0); } catch (const DomainError&) { threw = true; }
+        CHECK(threw);
+        threw = false;
+        try { signature_parallel(random_paths(140, 4, 32, 3, 1.0), 3, nullptr, 1000); } catch (const ResourceError&) { threw = true; }
+        CHECK(threw);
+        threw = false;
+        try { kernel_from_name("gpu"); } catch (const DomainError&) { threw = true; }
+        CHECK(threw);
+    }
+
+    std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
+    return failures ? 1 : 0;
+}
