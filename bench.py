@@ -208,8 +208,7 @@ def run_ours(args):
 
     st = sk.KernelStats()
     with torch.cuda.stream(stream):
-        sk.signature(pool[0], N, stats=st, out=out, chunks=TUNE.get("chunks", 0),
-                     prefix_len=TUNE.get("prefix_len", 0))
+        sk.signature(pool[0], N, stats=st, out=out, **TUNE)
     stream.synchronize()
 
     # FFMA-pipe peak on this GPU (roofline denominator)
@@ -253,8 +252,9 @@ def run_ours(args):
             _step(sk, pool[j % n_buf], N, out, None)
     stream.synchronize()
     reps_full, rem = divmod(args.steps, S)
-    g_main, ev_main = capture(S, True)
+    g_main = capture(S, False)[0]  # the timed graph carries no events (they would serialise launches)
     g_rem = capture(rem, False)[0] if rem else None
+    g_ev, ev_main = capture(S, True)  # kernel durations, replayed outside the timed region
     for _ in range(max(1, args.warmup // S)):
         g_main.replay()
     torch.cuda.synchronize()
@@ -275,6 +275,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier(world)
     elapsed = max_over_ranks(t0.elapsed_time(t1) * 1e-3, world)
+    with torch.cuda.stream(stream):
+        g_ev.replay()
+    stream.synchronize()
     fold_ms = [a.elapsed_time(b) for a, b in ev_main]
     fold_s = max_over_ranks(sum(fold_ms) / len(fold_ms) * 1e-3, world)
 
@@ -335,7 +338,7 @@ def run_ours(args):
     steps = args.steps
     value = world * B * steps / elapsed
     achieved = B * flops_path / (elapsed / steps) / 1e12
-    kernel_name = "flat_kernel" if st.threads_per_unit > 256 else "path_kernel"
+    kernel_name = {1: "path_kernel", 2: "flat_kernel", 3: "pair_kernel", 4: "generic_fold_kernel"}.get(st.family, "?")
     traffic = _traffic(args.config)
     peaks = load_peaks()
     line = {
@@ -359,6 +362,7 @@ def run_ours(args):
             "l2": f"inputs rotate over {n_buf} device batches = {n_buf * in_bytes / 2**20:.0f} MiB (> 126 MB L2)",
             "timing": f"{steps} steps = CUDA graph of {S} steps x {reps_full}"
                       + (f" + {rem}" if rem else "") + "; CUDA events on the launch stream; max over ranks",
+            "family": sk.FAMILY_NAMES.get(st.family, "?"), "segments": st.segments,
             "chunks": st.chunks, "prefix_len": st.prefix_len, "threads_per_unit": st.threads_per_unit,
             "fold_steps_per_unit": st.fold_steps, "merge_rounds": st.scan_passes,
             "single_launch_ms": single_ms,
@@ -366,8 +370,7 @@ def run_ours(args):
         },
         "roofline": {
             "bound": "fp32",
-            "kernel": f"{kernel_name} (the only kernel of a step; FFMA-pipe bound, tensor cores deliberately "
-                      "unused, SURVEY.md §8d)",
+            "kernel": f"{kernel_name} (FFMA-pipe bound; tensor cores deliberately unused, SURVEY.md §8d)",
             "achieved": achieved,
             "peak": peak,
             "unit": "TFLOP/s",
@@ -375,10 +378,14 @@ def run_ours(args):
             "frac_of_nominal": achieved / NOMINAL_FP32_TFLOPS,
             "peak_source": "measured: register-resident FFMA microbenchmark on this GPU (sigk_bench_ffma); "
                            f"nominal {NOMINAL_FP32_TFLOPS:.2f}",
-            "achieved_from": "credited flops per launch / mean launch interval of the timed back-to-back graph "
-                             "replays (one kernel per step, so this includes the inter-kernel gap)",
+            "achieved_from": "credited flops per step / mean step interval of the timed back-to-back graph "
+                             "replays (CUDA events around the timed region; includes every kernel of the step "
+                             "and the inter-kernel gaps)",
+            "kernels_per_step": st.launches,
             "credited_flops_per_launch": B * flops_path,
             "kernel_ms_event_bracketed": fold_s * 1e3,
+            "kernel_ms_event_bracketed_note": "fold kernel alone, events around every 4th launch of an untimed "
+                                              "replay (no launch overlap)",
             "hbm": {"algorithmic_bytes_per_launch": B * bytes_path,
                     "achieved_gbs": B * bytes_path / (elapsed / steps) / 1e9,
                     "peak_gbs": peaks.get("hbm_gbs"), "peak_source": "MEASURED_PEAKS.json"},
@@ -470,8 +477,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--chunks", type=int, default=0, help="force chunks per path (0: planned)")
     ap.add_argument("--prefix-len", type=int, default=0, help="force Q (0: planned)")
+    ap.add_argument("--segments", type=int, default=0, help="pair family: force CTAs per path (0: planned)")
+    ap.add_argument("--family", default="auto", choices=["auto", "path", "flat", "pair", "generic"])
     args = ap.parse_args()
-    TUNE.update(chunks=args.chunks, prefix_len=args.prefix_len)
+    fam = {"auto": 0, "path": 1, "flat": 2, "pair": 3, "generic": 4}[args.family]
+    TUNE.update(chunks=args.chunks, prefix_len=args.prefix_len, segments=args.segments, family=fam)
     if args.impl == "reference":
         args.steps = args.steps or 5
         args.warmup = 1 if args.warmup is None else args.warmup

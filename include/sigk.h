@@ -58,16 +58,25 @@ extern "C" {
 
 /* Structural counters (the reference KernelStats, kernels.hpp:86-91, plus
  * the GPU decomposition). fold_steps = increments folded by each (path,
- * chunk) unit = ceil((L-1)/chunks); scan_passes = depth of the Chen
- * merge tree = ceil(log2(chunks)). */
+ * chunk) unit = ceil((L-1)/(segments*chunks)); scan_passes = combine
+ * rounds = ceil(log2(chunks)) (+ ceil(log2(segments)) when segmented). */
 typedef struct sigk_stats {
     int64_t fold_steps;
     int64_t scan_passes;
-    int32_t chunks;       /* K: chunks per path along the sequence axis */
+    int32_t chunks;       /* K: chunks per segment along the sequence axis */
     int32_t prefix_len;   /* Q: leading indices owned per thread (-1: generic kernel) */
     int32_t threads_per_unit; /* d^Q */
     int32_t launches;     /* kernels launched by the call */
+    int32_t segments;     /* G: CTAs per path (pair family; 1 otherwise) */
+    int32_t family;       /* SIGK_FAMILY_* of the fold kernel */
 } sigk_stats;
+
+/* fold-kernel families (sigk_stats.family, sigk_tuning.family) */
+#define SIGK_FAMILY_AUTO 0    /* tuning: let the planner choose */
+#define SIGK_FAMILY_PATH 1    /* one CTA per path, scalar FFMA register slices (fp32/fp64) */
+#define SIGK_FAMILY_FLAT 2    /* warp-granular CTAs over path slices, no chunking (large d^N) */
+#define SIGK_FAMILY_PAIR 3    /* packed FP32x2 (FFMA2) chunk pairs, segment CTAs (fp32) */
+#define SIGK_FAMILY_GENERIC 4 /* shape-generic correctness kernel */
 
 /* Optional tuning overrides (NULL or zero fields = automatic). */
 typedef struct sigk_tuning {
@@ -87,7 +96,8 @@ typedef struct sigk_tuning {
                                sigk kernel on the same stream finishes (its output
                                writes still wait), unless X overlaps that kernel's
                                output. */
-    int32_t reserved[2];
+    int32_t segments;       /* pair family: force G >= 1 CTAs per path (0: planned) */
+    int32_t family;         /* SIGK_FAMILY_*: restrict the planner to one family (0: auto) */
     void* phase_buf;        /* optional device buffer of B*8 int64: per-CTA SM-clock
                                timestamps of the path kernel's phases (profiling) */
 } sigk_tuning;
@@ -117,6 +127,10 @@ int sigk_brownian_f64(double* X_dev, size_t B, size_t L, int d, uint64_t seed, s
 /* 1 when a register-sliced fast variant exists for (d, N) in this precision
  * (0: the shape-generic kernel is used). *Q receives the prefix length. */
 int sigk_has_fast_variant(int d, int N, int is_f64, int* Q);
+
+/* The launch plan sigk_signature_* would use for this shape on the current
+ * device (no kernel runs): family, Q, chunks, segments, fold_steps. */
+int sigk_plan(size_t B, size_t L, int d, int N, int is_f64, const sigk_tuning* tuning, sigk_stats* plan);
 
 /* FP32 FFMA-pipe peak microbenchmark (roofline denominator): launches
  * `blocks` x 256 threads, each running iters*128 independent-chain FFMAs;

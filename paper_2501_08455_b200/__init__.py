@@ -43,13 +43,15 @@ class DeviceError(RuntimeError):
 
 class _Stats(C.Structure):
     _fields_ = [("fold_steps", C.c_int64), ("scan_passes", C.c_int64), ("chunks", C.c_int32),
-                ("prefix_len", C.c_int32), ("threads_per_unit", C.c_int32), ("launches", C.c_int32)]
+                ("prefix_len", C.c_int32), ("threads_per_unit", C.c_int32), ("launches", C.c_int32),
+                ("segments", C.c_int32), ("family", C.c_int32)]
 
 
 class _Tuning(C.Structure):
     _fields_ = [("chunks", C.c_int32), ("force_generic", C.c_int32), ("plan_rows", C.c_int64),
                 ("fold_event_start", C.c_void_p), ("fold_event_stop", C.c_void_p), ("prefix_len", C.c_int32),
-                ("no_overlap", C.c_int32), ("reserved", C.c_int32 * 2), ("phase_buf", C.c_void_p)]
+                ("no_overlap", C.c_int32), ("segments", C.c_int32), ("family", C.c_int32),
+                ("phase_buf", C.c_void_p)]
 
 
 @dataclass
@@ -61,6 +63,13 @@ class KernelStats:
     prefix_len: int = 0
     threads_per_unit: int = 0
     launches: int = 0
+    segments: int = 0
+    family: int = 0
+
+
+# fold-kernel families (include/sigk.h SIGK_FAMILY_*)
+FAMILY_AUTO, FAMILY_PATH, FAMILY_FLAT, FAMILY_PAIR, FAMILY_GENERIC = 0, 1, 2, 3, 4
+FAMILY_NAMES = {0: "auto", 1: "path", 2: "flat", 3: "pair", 4: "generic"}
 
 
 class KernelKind(enum.Enum):
@@ -119,6 +128,7 @@ def lib():
         for n in ("sigk_brownian_f32", "sigk_brownian_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_uint64, sz, vp]
         L.sigk_has_fast_variant.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
+        L.sigk_plan.argtypes = [sz, sz, C.c_int, C.c_int, C.c_int, C.POINTER(_Tuning), C.POINTER(_Stats)]
         L.sigk_last_error.restype = C.c_char_p
         L.sigk_bench_ffma.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double), vp]
         _lib = L
@@ -178,10 +188,23 @@ def _validate_shape(shape, depth):
     return B, L, d
 
 
-def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_generic: bool = False,
-         out=None, plan_rows: int = 0, prefix_len: int = 0):
+def plan(B: int, L: int, d: int, depth: int, f64: bool = False, **tuning) -> KernelStats:
+    """The launch plan (family, Q, chunks, segments, steps per chunk) a call
+    would use on the current device; no kernel runs."""
     st = _Stats()
-    tun = _Tuning(chunks=chunks, force_generic=int(force_generic), plan_rows=plan_rows, prefix_len=prefix_len)
+    tun = _Tuning(**tuning)
+    _check(lib().sigk_plan(B, L, d, depth, int(f64), C.byref(tun), C.byref(st)))
+    ks = KernelStats()
+    for f, _ in _Stats._fields_:
+        setattr(ks, f, getattr(st, f))
+    return ks
+
+
+def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_generic: bool = False,
+         out=None, plan_rows: int = 0, prefix_len: int = 0, segments: int = 0, family: int = 0):
+    st = _Stats()
+    tun = _Tuning(chunks=chunks, force_generic=int(force_generic), plan_rows=plan_rows, prefix_len=prefix_len,
+                  segments=segments, family=family)
     if _is_torch(paths):
         import torch
 
@@ -217,16 +240,18 @@ def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_ge
 
 def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
               stats: KernelStats | None = None, *, chunks: int = 0, out=None, plan_rows: int = 0,
-              prefix_len: int = 0):
+              prefix_len: int = 0, segments: int = 0, family: int = 0):
     """Reference ``sigkit::signature`` (kernels.cpp:200-206): (B, L, d) -> (B, D).
 
     ``kernel``/``caps`` are accepted for source compatibility; every kind runs
     the same GPU kernels. ``chunks`` forces the sequence split (0 = planned);
     ``plan_rows`` plans the split as if the batch had that many rows (results
-    are bitwise independent of batch composition at equal chunking).
+    are bitwise independent of batch composition at equal chunking);
+    ``segments``/``family``/``prefix_len`` pin the rest of the plan (tests, tuning).
     """
     select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
-    return _run(paths, depth, stats, chunks=chunks, out=out, plan_rows=plan_rows, prefix_len=prefix_len)
+    return _run(paths, depth, stats, chunks=chunks, out=out, plan_rows=plan_rows, prefix_len=prefix_len,
+                segments=segments, family=family)
 
 
 def signature_sequential(paths, depth: int, stats: KernelStats | None = None, **kw):
@@ -280,5 +305,6 @@ __all__ = [
     "DomainError", "ResourceError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
-    "has_fast_variant", "lib",
+    "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
+    "FAMILY_GENERIC", "FAMILY_NAMES",
 ]

@@ -125,21 +125,94 @@ static double model_cycles(const Variant& v, int64_t B, int64_t M, int sms, int 
     return waves * (fold + merge + sync);
 }
 
+// Pair family (pair_kernel.cuh), modelled for back-to-back launches (the
+// serving / benchmark regime, where programmatic dependent launch keeps every
+// SM's CTA slots filled across calls): B*G segment CTAs of w = ceil(U/2*P/32)
+// warps; each CTA's fold keeps the FMA pipe busy for fold_pipe cycles (an
+// FFMA2 is 2 pipe cycles per warp) and spends `fixed` cycles in staging, table
+// build and chunk combine with the pipe mostly idle. With c CTAs resident per
+// SM the SM retires a CTA every max(pipe-bound, latency-bound) cycles.
+static double pair_eff(double warps_per_smsp) {
+    if (warps_per_smsp >= 3.0) return 0.92;
+    if (warps_per_smsp >= 2.0) return 0.85 + 0.07 * (warps_per_smsp - 2.0);
+    if (warps_per_smsp >= 1.0) return 0.6 + 0.25 * (warps_per_smsp - 1.0);
+    return 0.6 * warps_per_smsp;
+}
+
+static double model_pair(const Variant& v, int64_t B, int64_t M, int sms, int G, int U, int occ) {
+    const int64_t SL = (M + G - 1) / G;
+    const int64_t CL = (SL + U - 1) / U;
+    const int64_t ctas = B * G;
+    const int warps = (int)((U / 2 * v.P + 31) / 32);
+    const double fold_pipe = warps * (double)CL * v.ops * 2.0 / 4.0;
+    const double fixed = 2500.0 + 60.0 * U + 300.0 * v.N + 4.0 * CL;
+    const double c = (double)std::max(1, occ);
+    const double per_cta = std::max(fold_pipe / pair_eff(c * warps / 4.0),
+                                    (fixed + fold_pipe / pair_eff(warps / 4.0)) / c);
+    double t = (double)ctas / sms * per_cta;
+    if (G > 1) t += (double)B / sms * (1500.0 + 80.0 * G) + 1500.0;
+    return t;
+}
+
 struct Plan {
     const Variant* v = nullptr;
     int U = 1;
+    int G = 1;
 };
 
-// Pick the variant (prefix length Q) and chunks per path U for a launch.
-static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms, int64_t D) {
-    const Variant* cands[4];
-    const int nc = find_variants(d, N, is_f64, cands, 4);
+static const int kSegCands[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 112, 128,
+                                160, 192, 256, 320, 384, 512, 640, 768, 1024};
+
+// Pick the variant, chunks per path (or per segment) U and segments G.
+static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms, int64_t D, const sigk_tuning* tun) {
+    const Variant* cands[8];
+    const int nc = find_variants(d, N, is_f64, cands, 8);
+    const int fam = tun ? tun->family : 0;
+    const int fq = tun ? tun->prefix_len : 0;
+    const int fU = tun ? tun->chunks : 0;
+    const int fG = tun ? tun->segments : 0;
+    bool have_pair = false;
+    for (int k = 0; k < nc; ++k)
+        if (cands[k]->family == KernelFamily::Pair && (fam == 0 || fam == SIGK_FAMILY_PAIR) && (fq == 0 || fq == cands[k]->Q))
+            have_pair = true;
     Plan best;
     double best_t = 1e300;
     for (int k = 0; k < nc; ++k) {
         const Variant& v = *cands[k];
+        if (fam != 0 && (int)v.family != fam) continue;
+        if (fq > 0 && v.Q != fq) continue;
+        if (v.family == KernelFamily::Pair) {
+            const int gforce[1] = {fG};
+            const int* gl = fG > 0 ? gforce : kSegCands;
+            const int ng = fG > 0 ? 1 : (int)(sizeof(kSegCands) / sizeof(int));
+            for (int gi = 0; gi < ng; ++gi) {
+                const int G = gl[gi];
+                if (G > 1 && (N < 2 || (fG == 0 && (int64_t)G * 4 > M) || G > M)) continue;
+                const int64_t SL = (M + G - 1) / G;
+                const int umax = std::max(2, 2 * v.pair_units_max);
+                // a forced chunk count is rounded down to even (>= 2) and clamped to one CTA
+                const int uforce = fU > 0 ? std::min(umax, std::max(2, fU / 2 * 2)) : 0;
+                for (int U = 2; U <= umax; U += 2) {
+                    if (uforce > 0 && U != uforce) continue;
+                    if (uforce == 0 && U > 2 && U > SL + 1) break;  // whole empty pair-units
+                    const int CL = (int)((SL + U - 1) / U);
+                    int occ = 0;
+                    if (v.pair_occupancy(U, CL, SL, &occ) != cudaSuccess || occ < 1) continue;
+                    const double t = model_pair(v, B, M, sms, G, U, occ);
+                    if (t < best_t * 0.995) {
+                        best_t = t;
+                        best.v = &v;
+                        best.U = U;
+                        best.G = G;
+                    }
+                }
+            }
+            continue;
+        }
+        if (have_pair) continue;  // fp32 shapes with a pair variant use it
         const int umax = v.family == KernelFamily::Path ? (int)std::min<int64_t>(M, v.nt / v.P) : 1;
         for (int U = 1; U <= umax; ++U) {
+            if (fU > 0 && v.family == KernelFamily::Path && U != std::min<int64_t>(fU, umax)) continue;
             int occ = 0;
             if (v.occupancy(U, &occ) != cudaSuccess || occ < 1) continue;
             const double t = model_cycles(v, B, M, sms, U, occ, D);
@@ -147,6 +220,7 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
                 best_t = t;
                 best.v = &v;
                 best.U = U;
+                best.G = 1;
             }
         }
     }
@@ -157,21 +231,24 @@ struct PlanKey {
     int d, N, dev;
     bool f64;
     int64_t B, M;
+    int fam, q, U, G;
     bool operator==(const PlanKey& o) const {
-        return d == o.d && N == o.N && dev == o.dev && f64 == o.f64 && B == o.B && M == o.M;
+        return d == o.d && N == o.N && dev == o.dev && f64 == o.f64 && B == o.B && M == o.M && fam == o.fam &&
+               q == o.q && U == o.U && G == o.G;
     }
 };
 
-static Plan cached_plan(int d, int N, bool is_f64, int dev, int64_t B, int64_t M, int64_t D) {
+static Plan cached_plan(int d, int N, bool is_f64, int dev, int64_t B, int64_t M, int64_t D, const sigk_tuning* tun) {
     static std::mutex mu;
     static std::vector<std::pair<PlanKey, Plan>> cache;
-    const PlanKey key{d, N, dev, is_f64, B, M};
+    const PlanKey key{d, N, dev, is_f64, B, M, tun ? tun->family : 0, tun ? tun->prefix_len : 0,
+                      tun ? tun->chunks : 0, tun ? tun->segments : 0};
     {
         std::lock_guard<std::mutex> g(mu);
         for (auto& kv : cache)
             if (kv.first == key) return kv.second;
     }
-    const Plan p = plan_launch(d, N, is_f64, B, M, device_info(dev).sms, D);
+    const Plan p = plan_launch(d, N, is_f64, B, M, device_info(dev).sms, D, tun);
     std::lock_guard<std::mutex> g(mu);
     if (cache.size() > 256) cache.clear();
     cache.emplace_back(key, p);
@@ -211,6 +288,43 @@ static bool may_overlap_previous(int dev, cudaStream_t s, const void* X, size_t 
     return true;
 }
 
+// Per-(device, stream) scratch for segment results. Buffers are never freed
+// (a CUDA graph captured earlier may still reference them); they grow
+// geometrically. During stream capture a missing buffer is allocated
+// stream-ordered instead (and freed the same way by the caller).
+static void* segment_scratch(int dev, cudaStream_t s, size_t bytes, bool capturing, bool* async_alloc) {
+    struct Buf {
+        int dev;
+        cudaStream_t s;
+        void* p;
+        size_t n;
+    };
+    static std::mutex mu;
+    static std::vector<Buf> bufs;
+    *async_alloc = false;
+    std::lock_guard<std::mutex> g(mu);
+    Buf* hit = nullptr;
+    for (Buf& b : bufs)
+        if (b.dev == dev && b.s == s) hit = &b;
+    if (hit && hit->n >= bytes) return hit->p;
+    if (capturing) {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
+        *async_alloc = true;
+        return p;
+    }
+    const size_t n = std::max(bytes, hit ? 2 * hit->n : bytes);
+    void* p = nullptr;
+    if (cudaMalloc(&p, n) != cudaSuccess) return nullptr;
+    if (hit) {
+        hit->p = p;
+        hit->n = n;
+    } else {
+        bufs.push_back(Buf{dev, s, p, n});
+    }
+    return p;
+}
+
 template <typename Real>
 static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* out, cudaStream_t s,
                       const sigk_tuning* tun, sigk_stats* st) {
@@ -248,13 +362,8 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
     cudaGetDevice(&dev);
     const int64_t plan_rows = (tun && tun->plan_rows > 0) ? tun->plan_rows : B;
     Plan plan;
-    if (!(tun && tun->force_generic)) plan = cached_plan(d, N, is_f64, dev, plan_rows, M, D);
-    if (plan.v && tun && tun->prefix_len > 0) {  // pin Q (tests / tuning)
-        const Variant* cands[4];
-        const int nc = find_variants(d, N, is_f64, cands, 4);
-        for (int k = 0; k < nc; ++k)
-            if (cands[k]->Q == tun->prefix_len) plan.v = cands[k];
-    }
+    if (!(tun && (tun->force_generic || tun->family == SIGK_FAMILY_GENERIC)))
+        plan = cached_plan(d, N, is_f64, dev, plan_rows, M, D, tun);
     const Variant* v = plan.v;
     if (v == nullptr) {
         record(ev0);
@@ -266,6 +375,42 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         local.prefix_len = -1;
         local.threads_per_unit = 0;
         local.launches = 1;
+        local.segments = 1;
+        local.family = SIGK_FAMILY_GENERIC;
+        if (st) *st = local;
+        return SIGK_OK;
+    }
+    const bool overlap = !(tun && tun->no_overlap) &&
+                         may_overlap_previous(dev, s, X, sizeof(Real) * B * L * d, out, sizeof(Real) * B * D);
+    if (v->family == KernelFamily::Pair) {
+        const int G = plan.G, U = plan.U;
+        const int64_t SL = (M + G - 1) / G;
+        const int CL = (int)((SL + U - 1) / U);
+        void* scratch = nullptr;
+        bool async_alloc = false;
+        if (G > 1) {
+            if (cap == cudaStreamCaptureStatusNone) cudaStreamIsCapturing(s, &cap);
+            scratch = segment_scratch(dev, s, sizeof(float) * B * G * D, cap == cudaStreamCaptureStatusActive,
+                                      &async_alloc);
+            if (!scratch) return fail(SIGK_ERESOURCE, "segment scratch allocation failed");
+        }
+        PairLaunch a{X, B, L, G, SL, U, CL, out, scratch, s, overlap, ev0, ev1, cap == cudaStreamCaptureStatusActive,
+                     tun ? tun->phase_buf : nullptr};
+        e = v->pair_launch(a);
+        if (async_alloc) cudaFreeAsync(scratch, s);
+        if (e != cudaSuccess) return cuda_fail(e, "pair fold launch");
+        int rounds = 0;
+        while ((1 << rounds) < U) ++rounds;
+        int grounds = 0;
+        while ((1 << grounds) < G) ++grounds;
+        local.fold_steps = CL;
+        local.scan_passes = rounds + grounds;
+        local.chunks = U;
+        local.prefix_len = v->Q;
+        local.threads_per_unit = v->P;
+        local.launches = G > 1 ? 2 : 1;
+        local.segments = G;
+        local.family = SIGK_FAMILY_PAIR;
         if (st) *st = local;
         return SIGK_OK;
     }
@@ -282,8 +427,6 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         }
         if (occ < 1) return fail(SIGK_ERESOURCE, "fold variant does not fit on this device");
     }
-    const bool overlap = !(tun && tun->no_overlap) &&
-                         may_overlap_previous(dev, s, X, sizeof(Real) * B * L * d, out, sizeof(Real) * B * D);
     record(ev0);
     e = v->launch(X, B, L, U, out, s, tun ? tun->phase_buf : nullptr, overlap && !ev0);
     record(ev1);
@@ -297,6 +440,49 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
     local.prefix_len = v->Q;
     local.threads_per_unit = v->P;
     local.launches = 1;
+    local.segments = 1;
+    local.family = (int)v->family;
+    if (st) *st = local;
+    return SIGK_OK;
+}
+
+// The plan run_device would use (sigk_plan).
+static int plan_only(size_t B, size_t L, int d, int N, bool is_f64, const sigk_tuning* tun, sigk_stats* st) {
+    sigk_stats local{};
+    const int64_t M = (int64_t)L - 1;
+    int64_t D = 0, p = 1;
+    for (int n = 0; n < N; ++n) {
+        p *= d;
+        D += p;
+    }
+    local.segments = 1;
+    if (M <= 0) {
+        local.chunks = 1;
+        if (st) *st = local;
+        return SIGK_OK;
+    }
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    const int64_t plan_rows = (tun && tun->plan_rows > 0) ? tun->plan_rows : (int64_t)B;
+    Plan plan;
+    if (!(tun && (tun->force_generic || tun->family == SIGK_FAMILY_GENERIC)))
+        plan = cached_plan(d, N, is_f64, dev, plan_rows, M, D, tun);
+    if (!plan.v) {
+        local.family = SIGK_FAMILY_GENERIC;
+        local.prefix_len = -1;
+        local.chunks = 1;
+        local.fold_steps = M;
+    } else {
+        const int64_t SL = (M + plan.G - 1) / plan.G;
+        local.family = (int)plan.v->family;
+        local.prefix_len = plan.v->Q;
+        local.threads_per_unit = plan.v->P;
+        local.chunks = plan.U;
+        local.segments = plan.G;
+        local.fold_steps = (SL + plan.U - 1) / plan.U;
+        local.launches = plan.G > 1 ? 2 : 1;
+    }
     if (st) *st = local;
     return SIGK_OK;
 }
@@ -473,6 +659,12 @@ int sigk_brownian_f64(double* X, size_t B, size_t L, int d, uint64_t seed, size_
     return e == cudaSuccess ? SIGK_OK : sigk::cuda_fail(e, "brownian launch");
 }
 
+int sigk_plan(size_t B, size_t L, int d, int N, int is_f64, const sigk_tuning* tuning, sigk_stats* plan) {
+    sigk::g_err.clear();
+    if (B < 1 || L < 1 || d < 1 || N < 1) return sigk::fail(SIGK_EDOMAIN, "plan: bad shape");
+    return sigk::plan_only(B, L, d, N, is_f64 != 0, tuning, plan);
+}
+
 int sigk_has_fast_variant(int d, int N, int is_f64, int* Q) {
     const sigk::Variant* v = sigk::find_variant(d, N, is_f64 != 0);
     if (Q) *Q = v ? v->Q : -1;
@@ -481,7 +673,7 @@ int sigk_has_fast_variant(int d, int N, int is_f64, int* Q) {
 
 const char* sigk_last_error(void) { return sigk::g_err.c_str(); }
 
-int sigk_version(void) { return 100; }
+int sigk_version(void) { return 101; }
 
 }  // extern "C"
 

@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "flat_kernel.cuh"
+#include "pair_kernel.cuh"
 #include "path_kernel.cuh"
 #include "variants.h"
 
@@ -126,6 +127,89 @@ struct FlatVariant {
 template <typename Real, int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> FlatVariant<Real, DIM, DEPTH, Q>::smem_done{0};
 
+// Pair family (fp32 only): 256-thread CTAs, two per SM (<= 128 registers).
+template <int DIM, int DEPTH, int Q>
+struct PairVariant {
+    using PF = PairFold<DIM, DEPTH, Q>;
+    static constexpr int NT = 256;
+    static constexpr int MINB = 2;
+    static constexpr auto kernel = pair_kernel<DIM, DEPTH, Q, NT, MINB>;
+    static constexpr auto combine = segment_combine_kernel<DIM, DEPTH>;
+    static std::atomic<uint64_t> smem_done, comb_done;
+
+    static int raw_floats(int64_t SL) { return (int)(((SL + 1) * DIM + 3) / 4 * 4); }
+    static size_t smem(int U, int CL, int64_t SL) { return pair_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(SL)); }
+    static int threads(int U) { return (U / 2 * PF::P + 31) / 32 * 32; }
+    static size_t comb_smem(int G) { return CombineLayout<DIM, DEPTH>::floats(G, 0) * sizeof(float); }
+
+    static cudaError_t launch(const PairLaunch& a) {
+        PairGeom g;
+        g.G = a.G;
+        g.SL = a.SL;
+        g.U = a.U;
+        g.UP = a.U / 2;
+        g.CL = a.CL;
+        g.threads = threads(a.U);
+        g.raw_floats = raw_floats(a.SL);
+        g.phases = static_cast<long long*>(a.phases);
+        const size_t sm = smem(a.U, a.CL, a.SL);
+        cudaError_t e = opt_in_smem(kernel, sm, smem_done);
+        if (e != cudaSuccess) return e;
+        auto record = [&](void* ev) {
+            if (!ev) return;
+            if (a.capturing) cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), a.s, cudaEventRecordExternal);
+            else cudaEventRecord(static_cast<cudaEvent_t>(ev), a.s);
+        };
+        record(a.ev_fold_start);
+        float* dst = static_cast<float*>(a.G > 1 ? a.scratch : a.out);
+        e = launch_maybe_overlapped(kernel, dim3((unsigned)(a.B * a.G)), dim3(g.threads), sm, a.s,
+                                    a.overlap && !a.ev_fold_start, static_cast<const float*>(a.X), a.L, g, dst);
+        record(a.ev_fold_stop);
+        if (e != cudaSuccess || a.G == 1) return e;
+        const size_t cs = comb_smem(a.G);
+        e = opt_in_smem(combine, cs, comb_done);
+        if (e != cudaSuccess) return e;
+        return launch_maybe_overlapped(combine, dim3((unsigned)a.B), dim3(256), cs, a.s, true,
+                                       static_cast<const float*>(a.scratch), a.G, static_cast<float*>(a.out));
+    }
+    static cudaError_t occupancy(int U, int CL, int64_t SL, int* blocks) {
+        const size_t sm = smem(U, CL, SL);
+        *blocks = 0;
+        if (sm > 227 * 1024) return cudaSuccess;
+        cudaError_t e = opt_in_smem(kernel, sm, smem_done);
+        if (e != cudaSuccess) return e;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kernel, threads(U), sm);
+    }
+};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::smem_done{0};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::comb_done{0};
+
+// Smallest Q whose pair state (two chunks) fits ~80 registers, or -1.
+constexpr int pick_q_pair(int d, int N) {
+    for (int q = 0; q < N && q <= 2; ++q) {
+        int s = q > 1 ? q - 1 : 0;
+        for (int n = (q > 1 ? q : 1); n <= N; ++n) s += ipow(d, n - q);
+        if (2 * s <= 80 && ipow(d, q) <= 128) return q;
+    }
+    return -1;
+}
+
+template <int DIM, int DEPTH, int Q>
+Variant make_pair_variant() {
+    using PF = PairFold<DIM, DEPTH, Q>;
+    using V = PairVariant<DIM, DEPTH, Q>;
+    int chen = 0;
+    for (int n = 2; n <= DEPTH; ++n) chen += (n - 2) * ipow(DIM, n);
+    Variant v{DIM, DEPTH, Q, PF::P, PF::ops_per_step(), PF::loads_per_step(), chen, KernelFamily::Pair, V::NT, 0,
+              nullptr, nullptr};
+    v.pair_launch = &V::launch;
+    v.pair_occupancy = &V::occupancy;
+    v.pair_units_max = V::NT / PF::P;
+    return v;
+}
+
 template <typename Real, int DIM, int DEPTH, int Q>
 Variant make_variant() {
     using SF = SliceFold<Real, DIM, DEPTH, Q>;
@@ -135,11 +219,11 @@ Variant make_variant() {
     if constexpr (SF::P > 256) {
         using V = FlatVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Flat, V::NT, V::T,
-                       &V::launch, &V::occupancy};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0};
     } else {
         using V = PathVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Path, V::NTMAX, V::T,
-                       &V::launch, &V::occupancy};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0};
     }
 }
 
@@ -151,10 +235,13 @@ template <typename Real, int DIM, int DEPTH>
 struct VariantImpl {
     static constexpr int Q0 = pick_q<Real>(DIM, DEPTH);
     static constexpr bool SECOND = DIM > 1 && Q0 + 1 < DEPTH && ipow(DIM, Q0 + 1) <= 256 && ipow(DIM, Q0) <= 256;
-    static constexpr int count = SECOND ? 2 : 1;
+    static constexpr int QP = pick_q_pair(DIM, DEPTH);
+    static constexpr bool PAIR = sizeof(Real) == 4 && QP >= 0;
+    static constexpr int count = (SECOND ? 2 : 1) + (PAIR ? 1 : 0);
     static void fill(Variant* out) {
         out[0] = make_variant<Real, DIM, DEPTH, Q0>();
         if constexpr (SECOND) out[1] = make_variant<Real, DIM, DEPTH, Q0 + 1>();
+        if constexpr (PAIR) out[SECOND ? 2 : 1] = make_pair_variant<DIM, DEPTH, QP < 0 ? 0 : QP>();
     }
 };
 

@@ -7,7 +7,26 @@
 
 namespace sigk {
 
-enum class KernelFamily : int { Path = 0, Flat = 1 };
+enum class KernelFamily : int { Path = 1, Flat = 2, Pair = 3 };  // = SIGK_FAMILY_*
+
+// One launch of the pair family (pair_kernel.cuh): B*G CTAs of one path
+// segment each (SL steps as U chunks of CL), then, when G > 1, the segment
+// combine kernel from `scratch` ((B*G, D) floats) into `out`.
+struct PairLaunch {
+    const void* X;
+    int64_t B, L;
+    int G;
+    int64_t SL;
+    int U, CL;
+    void* out;
+    void* scratch;
+    cudaStream_t s;
+    bool overlap;
+    void* ev_fold_start;  // optional events recorded around the fold kernel
+    void* ev_fold_stop;
+    bool capturing;
+    void* phases;  // optional [B*G][8] int64 phase stamps
+};
 
 struct Variant {
     int d, N;
@@ -24,6 +43,10 @@ struct Variant {
                           bool overlap_previous);
     // resident CTAs per SM for a given U (0 when it does not fit)
     cudaError_t (*occupancy)(int U, int* blocks_per_sm);
+    // pair family only
+    cudaError_t (*pair_launch)(const PairLaunch& a);
+    cudaError_t (*pair_occupancy)(int U, int CL, int64_t SL, int* blocks_per_sm);  // 0 when it does not fit
+    int pair_units_max;  // max U/2 per CTA
 };
 
 const Variant* find_variant(int d, int N, bool is_f64);  // first (smallest-Q) candidate

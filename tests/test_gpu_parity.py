@@ -140,7 +140,7 @@ def test_ragged_lengths_and_chunk_counts(sk):
     for K in (1, 2, 3, 7, 16, 64, 256):
         st = sk.KernelStats()
         got = sk.signature(X, 4, chunks=K, stats=st)
-        assert 1 <= st.chunks <= K  # clamped to what fits one CTA
+        assert 1 <= st.chunks <= max(K, 2)  # clamped to what fits one CTA (pair family: even)
         assert max(level_errors(got, ref, 3, 4)) <= F64_TOL, K
         got32 = sk.signature(X.astype(np.float32), 4, chunks=K)
         assert max(level_errors(got32, O.signature(X.astype(np.float32).astype(np.float64), 4), 3, 4)) <= F32_TOL
