@@ -479,7 +479,10 @@ def main():
     ap.add_argument("--prefix-len", type=int, default=0, help="force Q (0: planned)")
     ap.add_argument("--segments", type=int, default=0, help="pair family: force CTAs per path (0: planned)")
     ap.add_argument("--family", default="auto", choices=["auto", "path", "flat", "pair", "generic"])
+    ap.add_argument("--shape", default="", help="experiments: override the config as B,L,d,N")
     args = ap.parse_args()
+    if args.shape:
+        CONFIGS[args.config] = tuple(int(x) for x in args.shape.split(","))
     fam = {"auto": 0, "path": 1, "flat": 2, "pair": 3, "generic": 4}[args.family]
     TUNE.update(chunks=args.chunks, prefix_len=args.prefix_len, segments=args.segments, family=fam)
     if args.impl == "reference":

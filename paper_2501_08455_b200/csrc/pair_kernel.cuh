@@ -679,7 +679,6 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
         }
     }
     phase(3);
-    pdl_wait();       // the previous launch has completed: output writes are ordered after its
     __syncthreads();  // table and staging are dead: reuse them for the combine
     phase(4);
     // 5. combine the U chunks
@@ -720,6 +719,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
     }
     __syncthreads();
     phase(6);
+    pdl_wait();  // the previous launch has completed: output writes are ordered after its
     const float* pU = S.pf + (size_t)U * DL;
     for (int i = tid; i < DL; i += nth) orow[i] = pU[i];
     sum_rows<LN, CLY::LNP>(S.red, UP, orow + DL);

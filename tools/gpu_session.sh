@@ -1,2 +1,1 @@
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1
-timeout 300 python tools/sweep.py c2 "family=auto" 5000 > gpurun_out/sweep_c2.txt 2>&1
+for f in 0 1 2 3 4 7; do echo "flags=$f"; SIGK_EXPERIMENT=$f timeout 300 python tools/sweep.py c2 "family=auto U=10,G=2 U=20,G=1" 5000 2>&1; done > gpurun_out/sweep_exp.txt

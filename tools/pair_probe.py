@@ -15,6 +15,7 @@ CFG = {"c1": (32, 100, 2, 4), "c2": (128, 1000, 5, 4), "c3": (128, 10000, 5, 4),
 name = sys.argv[1]
 combos = sys.argv[2].split() if len(sys.argv) > 2 else ["U=0"]
 B, L, d, N = CFG[name]
+pipelined = "pipe" in sys.argv[3:]  # 40 back-to-back launches (PDL overlap), stamps of the last ones
 for a in sys.argv[3:]:
     if a.startswith("B="):
         B = int(a[2:])
@@ -40,14 +41,20 @@ for combo in combos:
         e1.record()
         torch.cuda.synchronize()
         tun = sk._Tuning(family=3, **kw)
-        tun.fold_event_start = C.c_void_p(e0.cuda_event)
-        tun.fold_event_stop = C.c_void_p(e1.cuda_event)
+        if not pipelined:
+            tun.fold_event_start = C.c_void_p(e0.cuda_event)
+            tun.fold_event_stop = C.c_void_p(e1.cuda_event)
         tun.phase_buf = C.c_void_p(ph.data_ptr())
         st = sk._Stats()
-        sk._check(sk.lib().sigk_signature_f32(X.data_ptr(), B, L, d, N, out.data_ptr(), 3, C.c_void_p(s.cuda_stream),
-                                              C.byref(tun), C.byref(st)))
+        if pipelined:
+            e0.record()
+        for rep in range(40 if pipelined else 1):
+            sk._check(sk.lib().sigk_signature_f32(X.data_ptr(), B, L, d, N, out.data_ptr(), 3,
+                                                  C.c_void_p(s.cuda_stream), C.byref(tun), C.byref(st)))
+        if pipelined:
+            e1.record()
         torch.cuda.synchronize()
-        res.append(e0.elapsed_time(e1) * 1e3)
+        res.append(e0.elapsed_time(e1) * 1e3 / (40 if pipelined else 1))
     p = ph.cpu()
     dlt = (p[:, 1:8] - p[:, 0:7]).double().median(dim=0).values.tolist()
     start = p[:, 0].double()

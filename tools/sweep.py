@@ -8,12 +8,12 @@ import sys
 cfg = sys.argv[1]
 combos = sys.argv[2].split()
 steps = sys.argv[3] if len(sys.argv) > 3 else "5000"
-FLAG = {"U": "--chunks", "G": "--segments", "Q": "--prefix-len", "family": "--family"}
+FLAG = {"U": "--chunks", "G": "--segments", "Q": "--prefix-len", "family": "--family", "shape": "--shape"}
 for c in combos:
     extra = []
     for kv in c.split(","):
         k, v = kv.split("=")
-        extra += [FLAG[k], v]
+        extra += [FLAG[k], v.replace(":", ",")]
     r = subprocess.run([sys.executable, "bench.py", "--config", cfg, "--no-cpu", "--e2e-steps", "3", "--steps", steps]
                        + extra, capture_output=True, text=True)
     try:
