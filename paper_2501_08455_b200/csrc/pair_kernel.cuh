@@ -504,6 +504,50 @@ __device__ __forceinline__ void store_low_levels(const f2 (&st)[PF::S], int k, i
     }
 }
 
+// Segment combine of one path, run by the last of its G segment CTAs to
+// finish: rows Rb[g] (g = 0..G-1, written by the path's segment CTAs) are the
+// pieces of the combine above with P^(0)_1 = 0; the result goes to orow.
+// Loads bypass L1 (ld.global.cg): the rows were written by other SMs.
+template <int d, int N, bool P1S>
+__device__ __forceinline__ void segment_combine_path(const float* __restrict__ Rb, int G, float* __restrict__ smem,
+                                                     float* __restrict__ orow) {
+    using CLY = CombineLayout<d, N>;
+    constexpr int D = level_off(d, N), DL = CLY::DL, LN = CLY::LN;
+    CombineSmem<d, N, P1S> S(smem, G);
+    float* top = smem + CLY::floats(G, 0);  // [G][LN] level-N parts of the rows
+    const int tid = threadIdx.x, nth = blockDim.x;
+    // stage all G rows at once (every load in flight together; L2 reads)
+    for (int i = tid; i < G * D; i += nth) {
+        const int j = i / D, r = i - (i / D) * D;
+        const float v = __ldcg(Rb + i);
+        if (r < DL) S.ylow[(size_t)j * DL + r] = v;
+        else top[(size_t)j * LN + r - DL] = v;
+    }
+    if (tid < d) S.p10[tid] = 0.f;
+    __syncthreads();
+    fused_scan<d, N, P1S>(S, G, tid, nth);
+    build_c<d, N, P1S>(S, G, tid, nth);
+    __syncthreads();
+    const float* pG = S.pf + (size_t)G * DL;
+    for (int i = tid; i < DL; i += nth) orow[i] = pG[i];
+    for (int F = tid; F < LN; F += nth) {
+        float acc = 0.f;
+        for (int j = 0; j < G; ++j) {
+            float x = top[(size_t)j * LN + F];
+            if constexpr (N == 1 && P1S) {
+                if (j != G - 1) x = 0.f;
+            }
+#pragma unroll
+            for (int a = (P1S ? 2 : 1); a < N; ++a) {
+                const int tail = ipow(d, N - a);
+                x = fmaf(S.pf[(size_t)j * DL + level_off(d, a - 1) + F / tail], S.crow(j, N - a)[F % tail], x);
+            }
+            acc += x;
+        }
+        orow[DL + F] = acc;
+    }
+}
+
 // Geometry of one pair-kernel launch (host and device agree on it).
 struct PairGeom {
     int G;          // segments per path (grid = B * G)
@@ -512,14 +556,19 @@ struct PairGeom {
     int threads;    // block size (multiple of 32, >= UP * P)
     int raw_floats; // (SL + 1) * d rounded up to 4
     long long* phases;  // optional [grid][8] SM-clock stamps of thread 0 (tools/pair_probe.py)
+    int* counters;      // G > 1: [B] arrival counters (zero between launches)
+    int smem_bytes;     // dynamic shared memory of the launch (the last 16 bytes hold a flag)
+    float* final_out;   // G > 1: (B, D) signatures (the kernel's `out` then holds the (B*G, D) segment rows)
 };
 
 template <int d, int N, int Q>
-__host__ __device__ constexpr size_t pair_smem_bytes(int U, int CL, int raw_floats) {
+__host__ __device__ constexpr size_t pair_smem_bytes(int U, int CL, int raw_floats, int G = 1) {
     using PF = PairFold<d, N, Q>;
+    const size_t seg = G > 1 ? (CombineLayout<d, N>::floats(G, 0) + (size_t)G * ipow(d, N)) * 4 : 0;
     const size_t fold = (size_t)CL * (U / 2) * PF::RS * 8 + (size_t)raw_floats * 4 + 16 + 16;
     const size_t comb = CombineLayout<d, N>::floats(U, U / 2) * 4;
-    return fold > comb ? fold : comb;
+    const size_t m = fold > comb ? fold : comb;
+    return (m > seg ? m : seg) + 16;  // + the segment-combine flag
 }
 
 // X: (B, L, d) fp32. grid = B * G CTAs; CTA (b, g) folds steps
@@ -550,7 +599,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
     uint64_t* bar = reinterpret_cast<uint64_t*>(raw + g.raw_floats + 4);         // staging mbarrier
 
     auto phase = [&](int i) {
-        if (g.phases != nullptr && tid == 0) g.phases[rowid * 8 + i] = clock64();
+        if (g.phases != nullptr && tid == 0) g.phases[rowid * 10 + i] = clock64();
     };
     phase(0);
     pdl_trigger();  // the next launch may start on free SMs now
@@ -724,46 +773,22 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
     for (int i = tid; i < DL; i += nth) orow[i] = pU[i];
     sum_rows<LN, CLY::LNP>(S.red, UP, orow + DL);
     phase(7);
-}
-
-// Segment combine: R (B, G, D) segment results (pair_kernel rows) -> out (B, D).
-template <int DIM, int DEPTH, bool P1S = (DIM > 1)>
-__global__ void __launch_bounds__(256) segment_combine_kernel(const float* __restrict__ R, int G,
-                                                               float* __restrict__ out) {
-    using CLY = CombineLayout<DIM, DEPTH>;
-    constexpr int d = DIM, N = DEPTH;
-    constexpr int D = level_off(d, N), DL = CLY::DL, DC = CLY::DC, LN = CLY::LN;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    CombineSmem<d, N, P1S> S(reinterpret_cast<float*>(smem_raw), G);
-    const int64_t b = blockIdx.x;
-    const int tid = threadIdx.x, nth = blockDim.x;
-    pdl_trigger();
-    pdl_wait();  // R is the previous kernel's output
-    const float* Rb = R + b * G * D;
-    for (int i = tid; i < G * DL; i += nth) S.ylow[i] = Rb[(size_t)(i / DL) * D + i % DL];
-    if (tid < d) S.p10[tid] = 0.f;
-    __syncthreads();
-    fused_scan<d, N, P1S>(S, G, tid, nth);
-    build_c<d, N, P1S>(S, G, tid, nth);
-    __syncthreads();
-    float* orow = out + b * D;
-    const float* pG = S.pf + (size_t)G * DL;
-    for (int i = tid; i < DL; i += nth) orow[i] = pG[i];
-    for (int F = tid; F < LN; F += nth) {
-        float s = 0.f;
-        for (int j = 0; j < G; ++j) {
-            float x = Rb[(size_t)j * D + DL + F];
-            if constexpr (N == 1 && P1S) {
-                if (j != G - 1) x = 0.f;
-            }
-#pragma unroll
-            for (int a = (P1S ? 2 : 1); a < N; ++a) {
-                const int tail = ipow(d, N - a);
-                x = fmaf(S.pf[(size_t)j * DL + level_off(d, a - 1) + F / tail], S.crow(j, N - a)[F % tail], x);
-            }
-            s += x;
+    if (g.G > 1) {
+        // segment row written to scratch; the last of the path's G CTAs combines them
+        // (classic fence + counter: no second kernel, no grid-wide serialisation)
+        int* s_last = reinterpret_cast<int*>(smem_raw + g.smem_bytes - 16);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) *s_last = atomicAdd(g.counters + b, 1) == g.G - 1;
+        __syncthreads();
+        phase(8);
+        if (*s_last) {
+            __threadfence();
+            if (tid == 0) g.counters[b] = 0;  // ready for the next launch
+            segment_combine_path<d, N, P1S>(out + b * g.G * D, g.G, reinterpret_cast<float*>(smem_raw),
+                                            g.final_out + b * D);
         }
-        orow[DL + F] = s;
+        phase(9);
     }
 }
 

@@ -150,7 +150,7 @@ static double model_pair(const Variant& v, int64_t B, int64_t M, int sms, int G,
     const double per_cta = std::max(fold_pipe / pair_eff(c * warps / 4.0),
                                     (fixed + fold_pipe / pair_eff(warps / 4.0)) / c);
     double t = (double)ctas / sms * per_cta;
-    if (G > 1) t += (double)B / sms * (1500.0 + 80.0 * G) + 1500.0;
+    if (G > 1) t += (double)B / sms * (1000.0 + 60.0 * G);  // last-CTA segment combine
     return t;
 }
 
@@ -197,7 +197,7 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
                     if (uforce == 0 && U > 2 && U > SL + 1) break;  // whole empty pair-units
                     const int CL = (int)((SL + U - 1) / U);
                     int occ = 0;
-                    if (v.pair_occupancy(U, CL, SL, &occ) != cudaSuccess || occ < 1) continue;
+                    if (v.pair_occupancy(U, CL, SL, G, &occ) != cudaSuccess || occ < 1) continue;
                     const double t = model_pair(v, B, M, sms, G, U, occ);
                     if (t < best_t * 0.995) {
                         best_t = t;
@@ -249,6 +249,7 @@ static Plan cached_plan(int d, int N, bool is_f64, int dev, int64_t B, int64_t M
             if (kv.first == key) return kv.second;
     }
     const Plan p = plan_launch(d, N, is_f64, B, M, device_info(dev).sms, D, tun);
+    cudaGetLastError();  // occupancy probes of configurations that do not fit must not leak an error
     std::lock_guard<std::mutex> g(mu);
     if (cache.size() > 256) cache.clear();
     cache.emplace_back(key, p);
@@ -288,14 +289,17 @@ static bool may_overlap_previous(int dev, cudaStream_t s, const void* X, size_t 
     return true;
 }
 
-// Per-(device, stream) scratch for segment results. Buffers are never freed
-// (a CUDA graph captured earlier may still reference them); they grow
-// geometrically. During stream capture a missing buffer is allocated
-// stream-ordered instead (and freed the same way by the caller).
-static void* segment_scratch(int dev, cudaStream_t s, size_t bytes, bool capturing, bool* async_alloc) {
+// Per-(device, stream) scratch of the pair family's segmented plans: kind 0 =
+// segment rows, kind 1 = per-path arrival counters (zeroed when allocated and
+// left at zero by every completed launch). Buffers are never freed (a CUDA
+// graph captured earlier may still reference them) and grow geometrically.
+// During stream capture a missing buffer is allocated stream-ordered instead
+// (and freed the same way by the caller).
+static void* segment_scratch(int dev, cudaStream_t s, int kind, size_t bytes, bool capturing, bool* async_alloc) {
     struct Buf {
         int dev;
         cudaStream_t s;
+        int kind;
         void* p;
         size_t n;
     };
@@ -305,22 +309,24 @@ static void* segment_scratch(int dev, cudaStream_t s, size_t bytes, bool capturi
     std::lock_guard<std::mutex> g(mu);
     Buf* hit = nullptr;
     for (Buf& b : bufs)
-        if (b.dev == dev && b.s == s) hit = &b;
+        if (b.dev == dev && b.s == s && b.kind == kind) hit = &b;
     if (hit && hit->n >= bytes) return hit->p;
     if (capturing) {
         void* p = nullptr;
         if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
+        if (kind == 1 && cudaMemsetAsync(p, 0, bytes, s) != cudaSuccess) return nullptr;
         *async_alloc = true;
         return p;
     }
     const size_t n = std::max(bytes, hit ? 2 * hit->n : bytes);
     void* p = nullptr;
     if (cudaMalloc(&p, n) != cudaSuccess) return nullptr;
+    if (kind == 1 && cudaMemset(p, 0, n) != cudaSuccess) return nullptr;
     if (hit) {
         hit->p = p;
         hit->n = n;
     } else {
-        bufs.push_back(Buf{dev, s, p, n});
+        bufs.push_back(Buf{dev, s, kind, p, n});
     }
     return p;
 }
@@ -386,18 +392,21 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         const int G = plan.G, U = plan.U;
         const int64_t SL = (M + G - 1) / G;
         const int CL = (int)((SL + U - 1) / U);
-        void* scratch = nullptr;
-        bool async_alloc = false;
+        void* rows = nullptr;
+        void* counters = nullptr;
+        bool async_rows = false, async_ctr = false;
         if (G > 1) {
             if (cap == cudaStreamCaptureStatusNone) cudaStreamIsCapturing(s, &cap);
-            scratch = segment_scratch(dev, s, sizeof(float) * B * G * D, cap == cudaStreamCaptureStatusActive,
-                                      &async_alloc);
-            if (!scratch) return fail(SIGK_ERESOURCE, "segment scratch allocation failed");
+            const bool capt = cap == cudaStreamCaptureStatusActive;
+            rows = segment_scratch(dev, s, 0, sizeof(float) * B * G * D, capt, &async_rows);
+            counters = segment_scratch(dev, s, 1, sizeof(int) * B, capt, &async_ctr);
+            if (!rows || !counters) return fail(SIGK_ERESOURCE, "segment scratch allocation failed");
         }
-        PairLaunch a{X, B, L, G, SL, U, CL, out, scratch, s, overlap, ev0, ev1, cap == cudaStreamCaptureStatusActive,
-                     tun ? tun->phase_buf : nullptr};
+        PairLaunch a{X, B, L, G, SL, U, CL, out, rows, counters, s, overlap, ev0, ev1,
+                     cap == cudaStreamCaptureStatusActive, tun ? tun->phase_buf : nullptr};
         e = v->pair_launch(a);
-        if (async_alloc) cudaFreeAsync(scratch, s);
+        if (async_rows) cudaFreeAsync(rows, s);
+        if (async_ctr) cudaFreeAsync(counters, s);
         if (e != cudaSuccess) return cuda_fail(e, "pair fold launch");
         int rounds = 0;
         while ((1 << rounds) < U) ++rounds;
@@ -408,7 +417,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         local.chunks = U;
         local.prefix_len = v->Q;
         local.threads_per_unit = v->P;
-        local.launches = G > 1 ? 2 : 1;
+        local.launches = 1;
         local.segments = G;
         local.family = SIGK_FAMILY_PAIR;
         if (st) *st = local;
@@ -481,7 +490,7 @@ static int plan_only(size_t B, size_t L, int d, int N, bool is_f64, const sigk_t
         local.chunks = plan.U;
         local.segments = plan.G;
         local.fold_steps = (SL + plan.U - 1) / plan.U;
-        local.launches = plan.G > 1 ? 2 : 1;
+        local.launches = 1;
     }
     if (st) *st = local;
     return SIGK_OK;

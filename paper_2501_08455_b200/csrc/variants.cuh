@@ -134,13 +134,13 @@ struct PairVariant {
     static constexpr int NT = 256;
     static constexpr int MINB = 2;
     static constexpr auto kernel = pair_kernel<DIM, DEPTH, Q, NT, MINB>;
-    static constexpr auto combine = segment_combine_kernel<DIM, DEPTH>;
-    static std::atomic<uint64_t> smem_done, comb_done;
+    static std::atomic<uint64_t> smem_done;
 
     static int raw_floats(int64_t SL) { return (int)(((SL + 1) * DIM + 3) / 4 * 4); }
-    static size_t smem(int U, int CL, int64_t SL) { return pair_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(SL)); }
+    static size_t smem(int U, int CL, int64_t SL, int G) {
+        return pair_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(SL), G);
+    }
     static int threads(int U) { return (U / 2 * PF::P + 31) / 32 * 32; }
-    static size_t comb_smem(int G) { return CombineLayout<DIM, DEPTH>::floats(G, 0) * sizeof(float); }
 
     static cudaError_t launch(const PairLaunch& a) {
         PairGeom g;
@@ -152,7 +152,10 @@ struct PairVariant {
         g.threads = threads(a.U);
         g.raw_floats = raw_floats(a.SL);
         g.phases = static_cast<long long*>(a.phases);
-        const size_t sm = smem(a.U, a.CL, a.SL);
+        g.counters = static_cast<int*>(a.counters);
+        g.final_out = static_cast<float*>(a.out);
+        const size_t sm = smem(a.U, a.CL, a.SL, a.G);
+        g.smem_bytes = (int)sm;
         cudaError_t e = opt_in_smem(kernel, sm, smem_done);
         if (e != cudaSuccess) return e;
         auto record = [&](void* ev) {
@@ -165,15 +168,10 @@ struct PairVariant {
         e = launch_maybe_overlapped(kernel, dim3((unsigned)(a.B * a.G)), dim3(g.threads), sm, a.s,
                                     a.overlap && !a.ev_fold_start, static_cast<const float*>(a.X), a.L, g, dst);
         record(a.ev_fold_stop);
-        if (e != cudaSuccess || a.G == 1) return e;
-        const size_t cs = comb_smem(a.G);
-        e = opt_in_smem(combine, cs, comb_done);
-        if (e != cudaSuccess) return e;
-        return launch_maybe_overlapped(combine, dim3((unsigned)a.B), dim3(256), cs, a.s, true,
-                                       static_cast<const float*>(a.scratch), a.G, static_cast<float*>(a.out));
+        return e;
     }
-    static cudaError_t occupancy(int U, int CL, int64_t SL, int* blocks) {
-        const size_t sm = smem(U, CL, SL);
+    static cudaError_t occupancy(int U, int CL, int64_t SL, int G, int* blocks) {
+        const size_t sm = smem(U, CL, SL, G);
         *blocks = 0;
         if (sm > 227 * 1024) return cudaSuccess;
         cudaError_t e = opt_in_smem(kernel, sm, smem_done);
@@ -183,8 +181,6 @@ struct PairVariant {
 };
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::smem_done{0};
-template <int DIM, int DEPTH, int Q>
-std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::comb_done{0};
 
 // Smallest Q whose pair state (two chunks) fits ~80 registers, or -1.
 constexpr int pick_q_pair(int d, int N) {

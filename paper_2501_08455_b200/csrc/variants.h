@@ -10,8 +10,9 @@ namespace sigk {
 enum class KernelFamily : int { Path = 1, Flat = 2, Pair = 3 };  // = SIGK_FAMILY_*
 
 // One launch of the pair family (pair_kernel.cuh): B*G CTAs of one path
-// segment each (SL steps as U chunks of CL), then, when G > 1, the segment
-// combine kernel from `scratch` ((B*G, D) floats) into `out`.
+// segment each (SL steps as U chunks of CL). When G > 1 the segment rows go
+// to `scratch` ((B*G, D) floats) and the last segment CTA of each path (per
+// the zero-initialised `counters`, [B] ints) combines them into `out`.
 struct PairLaunch {
     const void* X;
     int64_t B, L;
@@ -20,6 +21,7 @@ struct PairLaunch {
     int U, CL;
     void* out;
     void* scratch;
+    void* counters;
     cudaStream_t s;
     bool overlap;
     void* ev_fold_start;  // optional events recorded around the fold kernel
@@ -45,7 +47,7 @@ struct Variant {
     cudaError_t (*occupancy)(int U, int* blocks_per_sm);
     // pair family only
     cudaError_t (*pair_launch)(const PairLaunch& a);
-    cudaError_t (*pair_occupancy)(int U, int CL, int64_t SL, int* blocks_per_sm);  // 0 when it does not fit
+    cudaError_t (*pair_occupancy)(int U, int CL, int64_t SL, int G, int* blocks_per_sm);  // 0: does not fit
     int pair_units_max;  // max U/2 per CTA
 };
 

@@ -58,7 +58,7 @@ def test_segments(sk, G):
     X = brownian(12, 1001, 5, seed=100 + G)
     ref = oracle32(X, 4)
     got, st = pair(sk, X, 4, segments=G)
-    assert st.segments == G and st.launches == 2
+    assert st.segments == G and st.launches == 1
     errs = level_errors(got, ref, 5, 4)
     assert max(errs) <= F32_TOL, errs
 

@@ -1,1 +1,1 @@
-for f in 0 1 2 3 4 7; do echo "flags=$f"; SIGK_EXPERIMENT=$f timeout 300 python tools/sweep.py c2 "family=auto U=10,G=2 U=20,G=1" 5000 2>&1; done > gpurun_out/sweep_exp.txt
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 4 -c 1 -o gpurun_out/pair_c2_full2 python tools/run_sig.py c2 6 > gpurun_out/ncu_full.log 2>&1

@@ -26,14 +26,14 @@ sk.brownian(X)
 D = sk.sig_dim(d, N)
 out = torch.empty((B, D), device="cuda")
 s = torch.cuda.current_stream()
-names = ["stage", "table", "fold", "pdl_wait", "scan", "top_cross", "out"]
+names = ["stage", "table", "fold", "pdl_wait", "scan", "top_cross", "out", "seg_fence", "seg_combine"]
 for combo in combos:
     kw = {}
     for kv in combo.split(","):
         k, v = kv.split("=")
         kw[{"U": "chunks", "G": "segments", "Q": "prefix_len"}[k]] = int(v)
     plan = sk.plan(B, L, d, N, family=3, **kw)
-    ph = torch.zeros((B * plan.segments, 8), dtype=torch.int64, device="cuda")
+    ph = torch.zeros((B * plan.segments, 10), dtype=torch.int64, device="cuda")
     res = []
     for it in range(5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -56,10 +56,14 @@ for combo in combos:
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1) * 1e3 / (40 if pipelined else 1))
     p = ph.cpu()
-    dlt = (p[:, 1:8] - p[:, 0:7]).double().median(dim=0).values.tolist()
+    if plan.segments == 1:
+        p[:, 8] = p[:, 7]
+        p[:, 9] = p[:, 7]
+    dlt = (p[:, 1:10] - p[:, 0:9]).double().median(dim=0).values.tolist()
     start = p[:, 0].double()
     rec = {"cfg": name, "B": B, "L": L, "G": st.segments, "U": st.chunks, "CL": st.fold_steps,
            "kernel_us": round(min(res), 2), "phase_cycles": dict(zip(names, [int(x) for x in dlt])),
-           "total_cycles": int((p[:, 7] - p[:, 0]).double().median().item()),
+           "total_cycles": int((p[:, 9] - p[:, 0]).double().median().item()),
+           "seg_combine_max": int((p[:, 9] - p[:, 8]).max().item()),
            "start_spread_cycles": int((start.max() - start.min()).item())}
     print(json.dumps(rec), flush=True)
