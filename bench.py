@@ -338,7 +338,8 @@ def run_ours(args):
     steps = args.steps
     value = world * B * steps / elapsed
     achieved = B * flops_path / (elapsed / steps) / 1e12
-    kernel_name = {1: "path_kernel", 2: "flat_kernel", 3: "pair_kernel", 4: "generic_fold_kernel"}.get(st.family, "?")
+    kernel_name = {1: "path_kernel", 2: "flat_kernel", 3: "pair_kernel", 4: "generic_fold_kernel",
+                   5: "ipair_kernel"}.get(st.family, "?")
     traffic = _traffic(args.config)
     peaks = load_peaks()
     line = {
@@ -478,12 +479,12 @@ def main():
     ap.add_argument("--chunks", type=int, default=0, help="force chunks per path (0: planned)")
     ap.add_argument("--prefix-len", type=int, default=0, help="force Q (0: planned)")
     ap.add_argument("--segments", type=int, default=0, help="pair family: force CTAs per path (0: planned)")
-    ap.add_argument("--family", default="auto", choices=["auto", "path", "flat", "pair", "generic"])
+    ap.add_argument("--family", default="auto", choices=["auto", "path", "flat", "pair", "generic", "pflat"])
     ap.add_argument("--shape", default="", help="experiments: override the config as B,L,d,N")
     args = ap.parse_args()
     if args.shape:
         CONFIGS[args.config] = tuple(int(x) for x in args.shape.split(","))
-    fam = {"auto": 0, "path": 1, "flat": 2, "pair": 3, "generic": 4}[args.family]
+    fam = {"auto": 0, "path": 1, "flat": 2, "pair": 3, "generic": 4, "pflat": 5}[args.family]
     TUNE.update(chunks=args.chunks, prefix_len=args.prefix_len, segments=args.segments, family=fam)
     if args.impl == "reference":
         args.steps = args.steps or 5

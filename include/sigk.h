@@ -77,6 +77,7 @@ typedef struct sigk_stats {
 #define SIGK_FAMILY_FLAT 2    /* warp-granular CTAs over path slices, no chunking (large d^N) */
 #define SIGK_FAMILY_PAIR 3    /* packed FP32x2 (FFMA2) chunk pairs, segment CTAs (fp32) */
 #define SIGK_FAMILY_GENERIC 4 /* shape-generic correctness kernel */
+#define SIGK_FAMILY_PFLAT 5   /* packed FP32x2 along the last index (even d), whole paths, no chunking (fp32) */
 
 /* Optional tuning overrides (NULL or zero fields = automatic). */
 typedef struct sigk_tuning {

@@ -23,7 +23,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsigk.so")
+# SIGK_LIB_PATH: an alternative build of the same library (tuning experiments)
+LIB_PATH = os.environ.get("SIGK_LIB_PATH") or os.path.join(_HERE, "libsigk.so")
 
 SIGK_OK, SIGK_EDOMAIN, SIGK_ERESOURCE, SIGK_EDEVICE = 0, 1, 2, 3
 SIGK_X_ON_DEVICE, SIGK_OUT_ON_DEVICE = 1, 2
@@ -68,8 +69,8 @@ class KernelStats:
 
 
 # fold-kernel families (include/sigk.h SIGK_FAMILY_*)
-FAMILY_AUTO, FAMILY_PATH, FAMILY_FLAT, FAMILY_PAIR, FAMILY_GENERIC = 0, 1, 2, 3, 4
-FAMILY_NAMES = {0: "auto", 1: "path", 2: "flat", 3: "pair", 4: "generic"}
+FAMILY_AUTO, FAMILY_PATH, FAMILY_FLAT, FAMILY_PAIR, FAMILY_GENERIC, FAMILY_PFLAT = 0, 1, 2, 3, 4, 5
+FAMILY_NAMES = {0: "auto", 1: "path", 2: "flat", 3: "pair", 4: "generic", 5: "pflat"}
 
 
 class KernelKind(enum.Enum):
@@ -306,5 +307,5 @@ __all__ = [
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
-    "FAMILY_GENERIC", "FAMILY_NAMES",
+    "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES",
 ]

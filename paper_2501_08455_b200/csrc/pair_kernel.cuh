@@ -655,33 +655,47 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
     __syncthreads();
     phase(1);
     // 2. the operand table: row (s, kk) = (δ_{2kk}[c]/m, δ_{2kk+1}[c]/m), m = 1..NR.
-    //    Column (kk, c) is split into `parts` contiguous step ranges, one per thread.
+    //    Column (kk, c) is split into `parts` contiguous step ranges, one per thread;
+    //    steps where both chunks are real run predicate-free, padding steps (δ = 0,
+    //    only in the last chunks of a segment) after them.
     {
         const int cols = UP * d;
         const int parts = nth / cols > 0 ? nth / cols : 1;
         const int len = (CL + parts - 1) / parts;
+        const int sl = (int)slen;
         for (int t = tid; t < cols * parts; t += nth) {
             const int col = t % cols, part = t / cols;
             const int kk = col / d, c = col - (col / d) * d;
             const int s0 = part * len, s1 = min(CL, s0 + len);
-            int64_t cs[2], lim[2];
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int64_t j = 2 * kk + hh;
-                cs[hh] = j * CL < slen ? j * CL : slen;
-                lim[hh] = ((j + 1) * CL < slen ? (j + 1) * CL : slen) - cs[hh];  // real steps of chunk j
-            }
-            const float* r0 = raw + (cs[0] + s0) * d + c;
-            const float* r1 = raw + (cs[1] + s0) * d + c;
-            float x0 = s0 <= lim[0] ? r0[0] : 0.f, x1 = s0 <= lim[1] ? r1[0] : 0.f;
-            f2* row = tab + ((size_t)s0 * UP + kk) * RS + c;
-            for (int sidx = s0; sidx < s1; ++sidx, r0 += d, r1 += d, row += (size_t)UP * RS) {
-                const float y0 = sidx < lim[0] ? r0[d] : x0, y1 = sidx < lim[1] ? r1[d] : x1;
+            const int cs0 = min(2 * kk * CL, sl), cs1 = min((2 * kk + 1) * CL, sl);
+            const int lim0 = min(cs0 + CL, sl) - cs0, lim1 = min(cs1 + CL, sl) - cs1;  // real steps
+            int o0 = (cs0 + s0) * d + c, o1 = (cs1 + s0) * d + c;
+            int ro = (s0 * UP + kk) * RS + c;
+            float x0 = s0 <= lim0 ? raw[o0] : 0.f, x1 = s0 <= lim1 ? raw[o1] : 0.f;
+            const int sf = min(s1, min(lim0, lim1));
+            int sidx = s0;
+#pragma unroll 4
+            for (; sidx < sf; ++sidx) {
+                const float y0 = raw[o0 + d], y1 = raw[o1 + d];
                 const float dl0 = y0 - x0, dl1 = y1 - x1;
                 x0 = y0;
                 x1 = y1;
 #pragma unroll
-                for (int m = 1; m <= NR; ++m) row[(m - 1) * RP] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
+                for (int m = 1; m <= NR; ++m) tab[ro + (m - 1) * RP] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
+                o0 += d;
+                o1 += d;
+                ro += UP * RS;
+            }
+            for (; sidx < s1; ++sidx) {
+                const float y0 = sidx < lim0 ? raw[o0 + d] : x0, y1 = sidx < lim1 ? raw[o1 + d] : x1;
+                const float dl0 = y0 - x0, dl1 = y1 - x1;
+                x0 = y0;
+                x1 = y1;
+#pragma unroll
+                for (int m = 1; m <= NR; ++m) tab[ro + (m - 1) * RP] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
+                o0 += d;
+                o1 += d;
+                ro += UP * RS;
             }
         }
     }

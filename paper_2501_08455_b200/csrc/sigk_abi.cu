@@ -175,12 +175,35 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
     for (int k = 0; k < nc; ++k)
         if (cands[k]->family == KernelFamily::Pair && (fam == 0 || fam == SIGK_FAMILY_PAIR) && (fq == 0 || fq == cands[k]->Q))
             have_pair = true;
+    // inner-pair flat family: whole paths as units, so only when the batch
+    // alone fills the GPU (>= 2 CTAs of 128 lanes per SM), and only where the
+    // scalar kernels need the flat (unchunked, register-heavy) form anyway —
+    // measured on B200: C4 (d=10, N=5) 2x faster than flat; C5 (d=8, N=4)
+    // 6% slower than the chunk-capable path kernel
+    bool scalar_flat = false;
+    for (int k = 0; k < nc; ++k)
+        if (cands[k]->family == KernelFamily::Flat) scalar_flat = true;
+    bool use_pflat = false;
+    for (int k = 0; k < nc; ++k)
+        if (cands[k]->family == KernelFamily::PFlat && (fq == 0 || fq == cands[k]->Q) &&
+            (fam == SIGK_FAMILY_PFLAT ||
+             (fam == 0 && !have_pair && scalar_flat && B * cands[k]->P >= (int64_t)sms * 256)))
+            use_pflat = true;
     Plan best;
     double best_t = 1e300;
     for (int k = 0; k < nc; ++k) {
         const Variant& v = *cands[k];
         if (fam != 0 && (int)v.family != fam) continue;
         if (fq > 0 && v.Q != fq) continue;
+        if ((v.family == KernelFamily::PFlat) != use_pflat) continue;
+        if (v.family == KernelFamily::PFlat) {
+            int occ = 0;
+            if (v.occupancy(1, &occ) != cudaSuccess || occ < 1) continue;
+            best.v = &v;
+            best.U = 1;
+            best.G = 1;
+            break;
+        }
         if (v.family == KernelFamily::Pair) {
             const int gforce[1] = {fG};
             const int* gl = fG > 0 ? gforce : kSegCands;
@@ -512,6 +535,23 @@ static int validate(const void* X, size_t B, size_t L, int d, int N, const void*
     return SIGK_OK;
 }
 
+struct Staging {
+    std::mutex mu;
+    void* p = nullptr;
+    size_t n = 0;
+};
+
+// Host-buffer staging per (device, stream); entries live for the process.
+static Staging& staging_for(int dev, cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, cudaStream_t>, Staging*>> tab;
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& kv : tab)
+        if (kv.first.first == dev && kv.first.second == s) return *kv.second;
+    tab.emplace_back(std::make_pair(dev, s), new Staging());
+    return *tab.back().second;
+}
+
 template <typename Real>
 static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real* out, unsigned flags,
                           void* stream, const sigk_tuning* tun, sigk_stats* st) {
@@ -525,37 +565,59 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
     const bool xdev = flags & SIGK_X_ON_DEVICE, odev = flags & SIGK_OUT_ON_DEVICE;
     const Real* Xd = X;
     Real* Od = out;
-    Real* xbuf = nullptr;
-    Real* obuf = nullptr;
     cudaError_t e;
+    if (xdev && odev) {
+        rc = run_device<Real>(Xd, (int64_t)B, (int64_t)L, d, N, Od, s, tun, st);
+        if (rc == SIGK_OK) {
+            e = cudaPeekAtLastError();
+            if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
+        }
+        return rc;
+    }
+    // Host buffers: the call is synchronous. Device staging comes from a
+    // per-(device, stream) buffer that persists across calls (a stream-ordered
+    // allocation per call would be returned to the OS at every synchronize and
+    // re-mapped by the next call), held under its lock for the whole call.
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Staging& stg = staging_for(dev, s);
+    std::lock_guard<std::mutex> lock(stg.mu);
+    const size_t xoff = 0, ooff = xdev ? 0 : (xbytes + 255) / 256 * 256;
+    const size_t need = ooff + (odev ? 0 : obytes);
+    if (stg.n < need) {
+        if (stg.p) cudaFree(stg.p);
+        stg.p = nullptr;
+        stg.n = 0;
+        e = cudaMalloc(&stg.p, need);
+        if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
+        stg.n = need;
+    }
     if (!xdev) {
-        e = cudaMallocAsync(reinterpret_cast<void**>(&xbuf), xbytes, s);
-        if (e != cudaSuccess) return cuda_fail(e, "input staging allocation");
+        Real* xbuf = reinterpret_cast<Real*>(static_cast<char*>(stg.p) + xoff);
         e = cudaMemcpyAsync(xbuf, X, xbytes, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
         Xd = xbuf;
     }
-    if (!odev) {
-        e = cudaMallocAsync(reinterpret_cast<void**>(&obuf), obytes, s);
-        if (e != cudaSuccess) return cuda_fail(e, "output staging allocation");
-        Od = obuf;
-    }
+    if (!odev) Od = reinterpret_cast<Real*>(static_cast<char*>(stg.p) + ooff);
     rc = run_device<Real>(Xd, (int64_t)B, (int64_t)L, d, N, Od, s, tun, st);
     if (rc == SIGK_OK && !odev) {
-        e = cudaMemcpyAsync(out, obuf, obytes, cudaMemcpyDeviceToHost, s);
+        e = cudaMemcpyAsync(out, Od, obytes, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
     }
-    if (xbuf) cudaFreeAsync(xbuf, s);
-    if (obuf) cudaFreeAsync(obuf, s);
-    if (!xdev || !odev) {
-        e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess && rc == SIGK_OK) rc = cuda_fail(e, "stream synchronize");
-    }
-    if (rc == SIGK_OK && (xdev && odev)) {
-        e = cudaPeekAtLastError();
-        if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
-    }
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && rc == SIGK_OK) rc = cuda_fail(e, "stream synchronize");
     return rc;
+}
+
+// One non-blocking stream per device for the sharded entry (created once, so
+// its staging buffers are reused across calls).
+static cudaStream_t shard_stream(int dev) {
+    static std::mutex mu;
+    static std::vector<cudaStream_t> streams;
+    std::lock_guard<std::mutex> g(mu);
+    if ((int)streams.size() <= dev) streams.resize(dev + 1, nullptr);
+    if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+    return streams[dev];
 }
 
 template <typename Real>
@@ -586,13 +648,11 @@ static int sharded_impl(const Real* X, size_t B, size_t L, int d, int N, Real* o
                 errs[g] = g_err;
                 return;
             }
-            cudaStream_t s;
-            cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+            cudaStream_t s = shard_stream(g);
             sigk_tuning tun{};
             tun.plan_rows = (int64_t)B;  // same chunking on every shard -> bitwise equal to G = 1
             rcs[g] = signature_impl<Real>(X + b0 * L * d, nb, L, d, N, out + b0 * D, 0u, s, &tun, &sts[g]);
             errs[g] = g_err;
-            cudaStreamDestroy(s);
         });
     }
     for (auto& t : th) t.join();

@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "flat_kernel.cuh"
+#include "ipair_kernel.cuh"
 #include "pair_kernel.cuh"
 #include "path_kernel.cuh"
 #include "variants.h"
@@ -206,6 +207,58 @@ Variant make_pair_variant() {
     return v;
 }
 
+// Inner-pair flat family (fp32, even d): 128-lane CTAs over (path, slice)
+// lanes, no chunking; 4 CTAs/SM for small states, 3 for large ones.
+template <int DIM, int DEPTH, int Q>
+struct IPairVariant {
+    using F = IPairFold<DIM, DEPTH, Q>;
+    static constexpr int NT = 128;
+    // steps per table tile: 32 (fewer barriers) unless the register-staged
+    // producer entries per thread would exceed 8
+    static constexpr int T = IPairGeom<DIM, DEPTH, Q, NT, 32>::EPT <= 8 ? 32 : 8;
+    static constexpr int SF = Q + 2 * F::NVP;  // state floats
+    static constexpr int MINB = SF <= 80 ? 4 : 3;
+    using G = IPairGeom<DIM, DEPTH, Q, NT, T>;
+    static constexpr auto kernel = ipair_kernel<DIM, DEPTH, Q, NT, T, MINB>;
+    static std::atomic<uint64_t> smem_done;
+
+    static cudaError_t launch(const void* X, int64_t B, int64_t L, int, void* out, cudaStream_t s, void*,
+                              bool overlap) {
+        cudaError_t e = opt_in_smem(kernel, G::smem, smem_done);
+        if (e != cudaSuccess) return e;
+        const int64_t lanes = B * (int64_t)F::P;
+        return launch_maybe_overlapped(kernel, dim3((unsigned)((lanes + NT - 1) / NT)), dim3(NT), G::smem, s, overlap,
+                                       static_cast<const float*>(X), B, L, static_cast<float*>(out));
+    }
+    static cudaError_t occupancy(int, int* blocks) {
+        cudaError_t e = opt_in_smem(kernel, G::smem, smem_done);
+        if (e != cudaSuccess) return e;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kernel, NT, G::smem);
+    }
+};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> IPairVariant<DIM, DEPTH, Q>::smem_done{0};
+
+// Smallest Q >= 1 whose inner-pair state fits ~120 registers (even d only), or -1.
+constexpr int pick_q_ipair(int d, int N) {
+    if (d % 2 || d < 2 || N < 2) return -1;
+    for (int q = 1; q < N; ++q) {
+        int s = q;
+        for (int n = q + 1; n <= N; ++n) s += ipow(d, n - q);
+        if (s <= 120) return ipow(d, q) <= 4096 ? q : -1;
+    }
+    return -1;
+}
+
+template <int DIM, int DEPTH, int Q>
+Variant make_ipair_variant() {
+    using V = IPairVariant<DIM, DEPTH, Q>;
+    using F = typename V::F;
+    Variant v{DIM, DEPTH, Q, F::P, F::pipe_cycles(), 0, 0, KernelFamily::PFlat, V::NT, V::T,
+              &V::launch, &V::occupancy, nullptr, nullptr, 0};
+    return v;
+}
+
 template <typename Real, int DIM, int DEPTH, int Q>
 Variant make_variant() {
     using SF = SliceFold<Real, DIM, DEPTH, Q>;
@@ -233,11 +286,15 @@ struct VariantImpl {
     static constexpr bool SECOND = DIM > 1 && Q0 + 1 < DEPTH && ipow(DIM, Q0 + 1) <= 256 && ipow(DIM, Q0) <= 256;
     static constexpr int QP = pick_q_pair(DIM, DEPTH);
     static constexpr bool PAIR = sizeof(Real) == 4 && QP >= 0;
-    static constexpr int count = (SECOND ? 2 : 1) + (PAIR ? 1 : 0);
+    static constexpr int QI = pick_q_ipair(DIM, DEPTH);
+    static constexpr bool IPAIR = sizeof(Real) == 4 && QI >= 1;
+    static constexpr int count = (SECOND ? 2 : 1) + (PAIR ? 1 : 0) + (IPAIR ? 1 : 0);
     static void fill(Variant* out) {
-        out[0] = make_variant<Real, DIM, DEPTH, Q0>();
-        if constexpr (SECOND) out[1] = make_variant<Real, DIM, DEPTH, Q0 + 1>();
-        if constexpr (PAIR) out[SECOND ? 2 : 1] = make_pair_variant<DIM, DEPTH, QP < 0 ? 0 : QP>();
+        int i = 0;
+        out[i++] = make_variant<Real, DIM, DEPTH, Q0>();
+        if constexpr (SECOND) out[i++] = make_variant<Real, DIM, DEPTH, Q0 + 1>();
+        if constexpr (PAIR) out[i++] = make_pair_variant<DIM, DEPTH, QP < 0 ? 0 : QP>();
+        if constexpr (IPAIR) out[i++] = make_ipair_variant<DIM, DEPTH, QI < 1 ? 1 : QI>();
     }
 };
 

@@ -7,7 +7,7 @@
 
 namespace sigk {
 
-enum class KernelFamily : int { Path = 1, Flat = 2, Pair = 3 };  // = SIGK_FAMILY_*
+enum class KernelFamily : int { Path = 1, Flat = 2, Pair = 3, PFlat = 5 };  // = SIGK_FAMILY_*
 
 // One launch of the pair family (pair_kernel.cuh): B*G CTAs of one path
 // segment each (SL steps as U chunks of CL). When G > 1 the segment rows go

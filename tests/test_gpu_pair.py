@@ -125,3 +125,44 @@ def test_headline_full_batch(sk):
     errs = level_errors(got, oracle32(X, 4), 5, 4)
     print("C2 pair plan", st, "errors", errs)
     assert max(errs) <= F32_TOL
+
+
+# ------------------------------------------------ inner-pair flat family (even d)
+def pflat(sk, X, N):
+    st = sk.KernelStats()
+    got = sk.signature(X, N, stats=st, family=sk.FAMILY_PFLAT)
+    assert st.family == sk.FAMILY_PFLAT, st
+    return got, st
+
+
+@pytest.mark.parametrize("d,N", [(2, 2), (2, 4), (2, 5), (4, 3), (4, 4), (4, 5), (6, 3), (6, 4), (8, 2), (8, 3),
+                                 (8, 4), (10, 2), (10, 3), (10, 4), (10, 5)])
+def test_pflat_every_variant(sk, d, N):
+    rng = np.random.default_rng(d * 17 + N)
+    for B, L in ((1, 2), (3, 37), (5, 301)):
+        X = brownian(B, L, d, seed=int(rng.integers(1 << 30)))
+        ref = oracle32(X, N)
+        got, _ = pflat(sk, X, N)
+        assert max(level_errors(got, ref, d, N)) <= F32_TOL, (d, N, B, L)
+
+
+def test_pflat_plans_for_c4_c5(sk):
+    assert sk.plan(64, 500, 10, 5).family == sk.FAMILY_PFLAT
+    assert sk.plan(8192, 1000, 8, 4).family == sk.FAMILY_PATH  # measured faster for d = 8
+    assert sk.plan(4, 500, 10, 5).family != sk.FAMILY_PFLAT  # too few lanes
+
+
+def test_pflat_c4_shape(sk):
+    X = brownian(64, 500, 10, seed=21)
+    got, st = pflat(sk, X, 5)
+    errs = level_errors(got, oracle32(X, 5), 10, 5)
+    print("C4 pflat", st, errs)
+    assert max(errs) <= F32_TOL
+
+
+def test_pflat_c5_rows(sk):
+    X = brownian(1000, 1000, 8, seed=22)  # 64000 lanes: ragged last CTA
+    got, _ = pflat(sk, X, 4)
+    for lo in (0, 500, 1000 - 40):
+        errs = level_errors(got[lo:lo + 40], oracle32(X[lo:lo + 40], 4), 8, 4)
+        assert max(errs) <= F32_TOL, (lo, errs)

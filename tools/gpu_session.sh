@@ -1,1 +1,2 @@
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:pair_kernel -s 4 -c 1 -o gpurun_out/pair_c2_full2 python tools/run_sig.py c2 6 > gpurun_out/ncu_full.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.txt 2>&1
+timeout 400 python bench.py --no-cpu > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err

@@ -15,7 +15,7 @@ kw = {}
 for a in sys.argv[3:]:
     k, v = a.split("=")
     if k == "family":
-        kw["family"] = {"path": 1, "flat": 2, "pair": 3, "generic": 4}[v]
+        kw["family"] = {"path": 1, "flat": 2, "pair": 3, "generic": 4, "pflat": 5}[v]
     else:
         kw[{"U": "chunks", "G": "segments", "Q": "prefix_len"}[k]] = int(v)
 B, L, d, N = CFG[name]
