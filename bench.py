@@ -44,6 +44,7 @@ CONFIGS = {
 }
 L2_BYTES = 126 * 1024 * 1024
 TUNE = {}  # sigk_tuning overrides from the command line (chunks / prefix_len)
+GRAPH_STEPS = int(os.environ.get("SIGK_BENCH_GRAPH_STEPS", "256"))  # steps captured per CUDA graph
 NOMINAL_FP32_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
@@ -229,7 +230,7 @@ def run_ours(args):
                 peak = max(peak, fl.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
 
     # graphs: S distinct steps per graph, every 4th step's fold kernel bracketed by events
-    S = min(args.steps, n_buf, 64)
+    S = min(args.steps, GRAPH_STEPS)
     step_events = []
 
     def capture(nsteps, with_events):

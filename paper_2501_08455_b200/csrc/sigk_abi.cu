@@ -536,9 +536,12 @@ static int validate(const void* X, size_t B, size_t L, int d, int N, const void*
 }
 
 struct Staging {
+    static constexpr int kPieces = 8;
     std::mutex mu;
     void* p = nullptr;
     size_t n = 0;
+    cudaStream_t hs = nullptr, ds = nullptr;  // H2D and D2H copy streams
+    cudaEvent_t ev[2 * kPieces + 2] = {};
 };
 
 // Host-buffer staging per (device, stream); entries live for the process.
@@ -567,7 +570,7 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
     Real* Od = out;
     cudaError_t e;
     if (xdev && odev) {
-        rc = run_device<Real>(Xd, (int64_t)B, (int64_t)L, d, N, Od, s, tun, st);
+        rc = run_device<Real>(Xd, (int64_t)B, (int64_t)L, d, N, Od, s, tun, st);  // asynchronous
         if (rc == SIGK_OK) {
             e = cudaPeekAtLastError();
             if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
@@ -578,6 +581,11 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
     // per-(device, stream) buffer that persists across calls (a stream-ordered
     // allocation per call would be returned to the OS at every synchronize and
     // re-mapped by the next call), held under its lock for the whole call.
+    // The batch is cut into row pieces so PCIe and compute overlap: all H2D
+    // copies go back to back on a copy stream, piece i's kernel waits only for
+    // its own rows, and its D2H runs on a third stream while later pieces copy
+    // in and fold (plan_rows = B keeps the plan, hence the results, identical
+    // to a single launch over the whole batch).
     int dev = 0;
     cudaGetDevice(&dev);
     Staging& stg = staging_for(dev, s);
@@ -592,20 +600,52 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
         if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
         stg.n = need;
     }
-    if (!xdev) {
-        Real* xbuf = reinterpret_cast<Real*>(static_cast<char*>(stg.p) + xoff);
-        e = cudaMemcpyAsync(xbuf, X, xbytes, cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-        Xd = xbuf;
+    if (!stg.hs) {
+        cudaStreamCreateWithFlags(&stg.hs, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&stg.ds, cudaStreamNonBlocking);
+        for (auto& ev : stg.ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     }
-    if (!odev) Od = reinterpret_cast<Real*>(static_cast<char*>(stg.p) + ooff);
-    rc = run_device<Real>(Xd, (int64_t)B, (int64_t)L, d, N, Od, s, tun, st);
-    if (rc == SIGK_OK && !odev) {
-        e = cudaMemcpyAsync(out, Od, obytes, cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
+    Real* xbuf = xdev ? const_cast<Real*>(X) : reinterpret_cast<Real*>(static_cast<char*>(stg.p) + xoff);
+    Real* obuf = odev ? out : reinterpret_cast<Real*>(static_cast<char*>(stg.p) + ooff);
+    // pieces pay off once PCIe time dwarfs the per-piece API cost (~8 MB each)
+    const size_t moved = (xdev ? 0 : xbytes) + (odev ? 0 : obytes);
+    const int np = (int)std::max<size_t>(1, std::min<size_t>({(size_t)Staging::kPieces, B / 32, moved >> 23}));
+    const size_t per = (B + np - 1) / np;
+    // the copy streams start after everything already queued on the caller's stream
+    cudaEventRecord(stg.ev[2 * Staging::kPieces], s);
+    cudaStreamWaitEvent(stg.hs, stg.ev[2 * Staging::kPieces], 0);
+    cudaStreamWaitEvent(stg.ds, stg.ev[2 * Staging::kPieces], 0);
+    sigk_tuning tp = tun ? *tun : sigk_tuning{};
+    if (tp.plan_rows <= 0) tp.plan_rows = (int64_t)B;
+    sigk_stats acc{};
+    int launches = 0;
+    for (int i = 0; i < np && rc == SIGK_OK; ++i) {
+        const size_t r0 = i * per, nr = std::min(per, B - r0);
+        if (nr == 0) break;
+        if (!xdev) {
+            e = cudaMemcpyAsync(xbuf + r0 * L * d, X + r0 * L * d, sizeof(Real) * nr * L * d, cudaMemcpyHostToDevice,
+                                stg.hs);
+            if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+            cudaEventRecord(stg.ev[i], stg.hs);
+            cudaStreamWaitEvent(s, stg.ev[i], 0);
+        }
+        rc = run_device<Real>(xbuf + r0 * L * d, (int64_t)nr, (int64_t)L, d, N, obuf + r0 * D, s, &tp, &acc);
+        launches += acc.launches;
+        if (rc == SIGK_OK && !odev) {
+            cudaEventRecord(stg.ev[Staging::kPieces + i], s);
+            cudaStreamWaitEvent(stg.ds, stg.ev[Staging::kPieces + i], 0);
+            e = cudaMemcpyAsync(out + r0 * D, obuf + r0 * D, sizeof(Real) * nr * D, cudaMemcpyDeviceToHost, stg.ds);
+            if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
+        }
     }
+    cudaEventRecord(stg.ev[2 * Staging::kPieces + 1], stg.ds);
+    cudaStreamWaitEvent(s, stg.ev[2 * Staging::kPieces + 1], 0);
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess && rc == SIGK_OK) rc = cuda_fail(e, "stream synchronize");
+    if (st) {
+        *st = acc;
+        st->launches = launches;
+    }
     return rc;
 }
 
