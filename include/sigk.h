@@ -12,6 +12,10 @@
  *   sigk_signature_f32    ← detail::sequential_forward<float>
  *                           include/sigkit/detail/sig_core.hpp:120-147 (the raw-pointer core the
  *                           reference bench instantiates for float, src/bench.cpp:29-56)
+ *   sigk_signature_stream_f32/_f64
+ *                         ← sigkit::signature_stream  include/sigkit/kernels.hpp:110-114,
+ *                           src/kernels.cpp:156-198 (every prefix signature, (B, L-1, D);
+ *                           row t = signature of X[0..t+1]; L < 2 is a DomainError)
  *   sigk_signature_sharded_f32/_f64
  *                         ← signature() over a batch split across GPUs (rows are independent,
  *                           SPEC.md:220-221; tests/test_kernels.cpp:252-263)
@@ -110,6 +114,14 @@ int sigk_signature_f32(const float* X, size_t B, size_t L, int d, int N, float* 
                        void* stream, const sigk_tuning* tuning, sigk_stats* stats);
 int sigk_signature_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags,
                        void* stream, const sigk_tuning* tuning, sigk_stats* stats);
+
+/* Prefix signatures: out is (B, L-1, D), row (b, t) = signature of
+ * X[b, 0..t+1] (the reference's PrefixSignatureBatch layout). L < 2 returns
+ * SIGK_EDOMAIN like the reference. Flags and stream as for sigk_signature_*. */
+int sigk_signature_stream_f32(const float* X, size_t B, size_t L, int d, int N, float* out, unsigned flags,
+                              void* stream, const sigk_tuning* tuning, sigk_stats* stats);
+int sigk_signature_stream_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags,
+                              void* stream, const sigk_tuning* tuning, sigk_stats* stats);
 
 /* Host buffers in and out; rows [g*ceil(B/G), ...) run on device g, one host
  * thread per device, each shard copied in, folded and copied back into its

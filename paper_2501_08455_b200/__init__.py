@@ -124,6 +124,9 @@ def lib():
         for n in ("sigk_signature_f32", "sigk_signature_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, C.c_uint, vp, C.POINTER(_Tuning),
                                       C.POINTER(_Stats)]
+        for n in ("sigk_signature_stream_f32", "sigk_signature_stream_f64"):
+            getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, C.c_uint, vp, C.POINTER(_Tuning),
+                                      C.POINTER(_Stats)]
         for n in ("sigk_signature_sharded_f32", "sigk_signature_sharded_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, C.c_int, C.POINTER(_Stats)]
         for n in ("sigk_brownian_f32", "sigk_brownian_f64"):
@@ -255,6 +258,44 @@ def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: Exe
                 segments=segments, family=family)
 
 
+def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
+                     stats: KernelStats | None = None, *, out=None, family: int = 0):
+    """Reference ``sigkit::signature_stream`` (kernels.cpp:156-198): (B, L, d) -> (B, L-1, D),
+    row (b, t) = signature of X[b, 0..t+1]. L < 2 raises DomainError."""
+    select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
+    st = _Stats()
+    tun = _Tuning(family=family)
+    if _is_torch(paths):
+        import torch
+
+        if not paths.is_cuda:
+            raise DomainError("torch input must be a CUDA tensor (use numpy for host buffers)")
+        B, L, d = _validate_shape(paths.shape, depth)
+        X = paths.contiguous()
+        D = sig_dim(d, depth)
+        if out is None:
+            out = torch.empty((B, max(L - 1, 0), D), dtype=X.dtype, device=X.device)
+        fn = lib().sigk_signature_stream_f32 if X.dtype == torch.float32 else lib().sigk_signature_stream_f64
+        with torch.cuda.device(X.device):
+            s = torch.cuda.current_stream(X.device).cuda_stream
+            _check(fn(X.data_ptr(), B, L, d, depth, out.data_ptr(), SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE,
+                      s, C.byref(tun), C.byref(st)))
+    else:
+        X = np.asarray(paths)
+        B, L, d = _validate_shape(X.shape, depth)
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        X = np.ascontiguousarray(X)
+        D = sig_dim(d, depth)
+        out = np.empty((B, max(L - 1, 0), D), dtype=X.dtype) if out is None else out
+        fn = lib().sigk_signature_stream_f32 if X.dtype == np.float32 else lib().sigk_signature_stream_f64
+        _check(fn(X.ctypes.data, B, L, d, depth, out.ctypes.data, 0, None, C.byref(tun), C.byref(st)))
+    if stats is not None:
+        for f, _ in _Stats._fields_:
+            setattr(stats, f, getattr(st, f))
+    return out
+
+
 def signature_sequential(paths, depth: int, stats: KernelStats | None = None, **kw):
     """Reference ``signature_sequential`` (kernels.cpp:106-122)."""
     return _run(paths, depth, stats, **kw)
@@ -306,6 +347,7 @@ __all__ = [
     "DomainError", "ResourceError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
+    "signature_stream",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
     "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES",
 ]

@@ -107,3 +107,61 @@ __global__ void brownian_kernel(Real* __restrict__ X, int64_t B, int64_t L, int 
 }
 
 }  // namespace sigk
+
+namespace sigk {
+
+// Prefix stream for shapes / precisions without the pair-family stream kernel:
+// out (B, L-1, D), row t = signature of X[0..t+1]. Row t is computed from row
+// t-1 (element-parallel, one barrier per step, no level ordering needed since
+// the previous state is a separate row):
+//     T_n(t)[I] = T_n(t-1)[I] + Σ_{j=1}^{n} T_{n-j}(t-1)[I / d^j] · Π_{last j digits c} δ[c] / j!
+template <typename Real>
+__global__ void __launch_bounds__(256) generic_stream_kernel(const Real* __restrict__ X, int64_t L, int d, int N,
+                                                             int64_t D, Real* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* dl = reinterpret_cast<Real*>(smem_raw);  // [d]
+    __shared__ int64_t off[kGenericMaxDepth + 1];
+    __shared__ Real invfact[kGenericMaxDepth + 1];
+    const int64_t b = blockIdx.x;
+    const int64_t M = L - 1;
+    Real* ob = out + b * M * D;
+    if (threadIdx.x == 0) {
+        off[0] = 0;
+        int64_t p = 1;
+        Real f = 1;
+        invfact[0] = 1;
+        for (int n = 1; n <= N; ++n) {
+            p *= d;
+            off[n] = off[n - 1] + p;
+            f *= Real(n);
+            invfact[n] = Real(1) / f;
+        }
+    }
+    pdl_trigger();
+    pdl_wait();
+    const Real* row = X + b * L * d;
+    for (int64_t t = 0; t < M; ++t) {
+        __syncthreads();
+        for (int c = threadIdx.x; c < d; c += blockDim.x) dl[c] = row[(t + 1) * d + c] - row[t * d + c];
+        __syncthreads();
+        const Real* prev = t > 0 ? ob + (t - 1) * D : nullptr;
+        Real* cur = ob + t * D;
+        for (int64_t F = threadIdx.x; F < D; F += blockDim.x) {
+            int n = 1;
+            while (F >= off[n]) ++n;
+            const int64_t I = F - off[n - 1];
+            Real acc = prev ? prev[F] : Real(0);
+            Real e = 1;
+            int64_t rem = I;
+            for (int j = 1; j <= n; ++j) {
+                e *= dl[rem % d];
+                rem /= d;
+                const Real lower = (j < n) ? (prev ? prev[off[n - j - 1] + rem] : Real(0)) : Real(1);
+                acc = fma(lower, e * invfact[j], acc);
+            }
+            cur[F] = acc;
+        }
+    }
+}
+
+}  // namespace sigk

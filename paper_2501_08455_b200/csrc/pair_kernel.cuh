@@ -20,8 +20,9 @@
 //    single barrier; the fold itself then runs barrier-free from registers
 //    and 16-byte broadcast loads of the table.
 //  * Segments. Long paths are split into G segments of one CTA each; a CTA
-//    returns R = A_seg ⊠ C_seg and a small second kernel (segment_combine)
-//    applies the same combine across segments.
+//    writes R = A_seg ⊠ C_seg to scratch and the last segment CTA of the path
+//    to finish (fence + per-path counter) applies the same combine across
+//    the G segment rows.
 //  * Chunk starts. Chunk j folds from A = (1, X[s_j] - X[0], 0, ..., 0)
 //    instead of the identity: the fold is S <- S ⊠ exp(δ) so it yields
 //    Y = A ⊠ C (Chen, tensor_algebra.cpp:80-102) at no extra cost, and the
@@ -293,6 +294,7 @@ struct CombineSmem {
     float* cm;    // [U][DC]  C^(j)_m, m = 1..N-2 (P1S only)
     float* pf;    // [U+1][DL] P^(j), levels < N
     float* red;   // [rows][LNP]
+    const float* p0 = nullptr;  // levels 2..N-1 of P^(0) (row layout, DL floats); null: zero
     __device__ CombineSmem(float* base, int U) {
         ylow = base;
         p10 = ylow + (size_t)U * CL_::DL;
@@ -381,7 +383,7 @@ __device__ __forceinline__ void fused_scan(const CombineSmem<d, N, P1S>& S, int 
             for (int a = A0; a <= E; ++a) {
                 idx[a] = I / ipow(d, E - a);
                 wr[a] = I % ipow(d, E - a) == 0;
-                P[a] = (a == 1) ? S.p10[idx[1]] : 0.f;
+                P[a] = (a == 1) ? S.p10[idx[1]] : (S.p0 ? S.p0[level_off(d, a - 1) + idx[a]] : 0.f);
                 if (wr[a]) S.pf[level_off(d, a - 1) + idx[a]] = P[a];
             }
 #pragma unroll 4
@@ -548,73 +550,16 @@ __device__ __forceinline__ void segment_combine_path(const float* __restrict__ R
     }
 }
 
-// Geometry of one pair-kernel launch (host and device agree on it).
-struct PairGeom {
-    int G;          // segments per path (grid = B * G)
-    int64_t SL;     // steps per segment
-    int U, UP, CL;  // chunks per segment (even), pair-units, steps per chunk
-    int threads;    // block size (multiple of 32, >= UP * P)
-    int raw_floats; // (SL + 1) * d rounded up to 4
-    long long* phases;  // optional [grid][8] SM-clock stamps of thread 0 (tools/pair_probe.py)
-    int* counters;      // G > 1: [B] arrival counters (zero between launches)
-    int smem_bytes;     // dynamic shared memory of the launch (the last 16 bytes hold a flag)
-    float* final_out;   // G > 1: (B, D) signatures (the kernel's `out` then holds the (B*G, D) segment rows)
-};
-
-template <int d, int N, int Q>
-__host__ __device__ constexpr size_t pair_smem_bytes(int U, int CL, int raw_floats, int G = 1) {
-    using PF = PairFold<d, N, Q>;
-    const size_t seg = G > 1 ? (CombineLayout<d, N>::floats(G, 0) + (size_t)G * ipow(d, N)) * 4 : 0;
-    const size_t fold = (size_t)CL * (U / 2) * PF::RS * 8 + (size_t)raw_floats * 4 + 16 + 16;
-    const size_t comb = CombineLayout<d, N>::floats(U, U / 2) * 4;
-    const size_t m = fold > comb ? fold : comb;
-    return (m > seg ? m : seg) + 16;  // + the segment-combine flag
-}
-
-// X: (B, L, d) fp32. grid = B * G CTAs; CTA (b, g) folds steps
-// [g*SL, min((g+1)*SL, M)) of path b as U chunks and writes row b*G + g of
-// `out` ((B*G, D)): A_seg ⊠ C_seg with A_seg = (1, X[seg start] - X[0], 0, ...),
-// i.e. the path's signature when G == 1.
-template <int DIM, int DEPTH, int Q, int NT, int MINB, bool P1S = (DIM > 1)>
-__global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict__ X, int64_t L, PairGeom g,
-                                                        float* __restrict__ out) {
-    using PF = PairFold<DIM, DEPTH, Q>;
-    using CLY = CombineLayout<DIM, DEPTH>;
-    constexpr int d = DIM, N = DEPTH, P = PF::P, RS = PF::RS, RP = PF::RP, NR = PF::NR;
-    constexpr int D = level_off(DIM, DEPTH);
-    constexpr int DL = CLY::DL, DC = CLY::DC, LN = CLY::LN, FJ = PF::FJ;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-
-    const int64_t rowid = blockIdx.x;
-    const int64_t b = rowid / g.G, sg = rowid - b * g.G;
-    const int64_t M = L - 1;
-    const int64_t seg0 = sg * g.SL < M ? sg * g.SL : M;
-    const int64_t slen = (seg0 + g.SL < M ? seg0 + g.SL : M) - seg0;
-    const int U = g.U, UP = g.UP, CL = g.CL;
+// Steps 1-2 of a pair-family CTA (also used by the prefix-stream kernel):
+// stage the segment's points X[seg0 .. seg0+slen] into `raw` and build the
+// δ table `tab` ([CL][UP][RS] pairs). Returns the (shifted) raw pointer. The
+// table is complete after the caller's next __syncthreads().
+template <typename PF>
+__device__ __forceinline__ float* pair_stage_and_table(const float* __restrict__ xb, int64_t seg0, int64_t slen,
+                                                       int CL, int UP, f2* __restrict__ tab, float* raw,
+                                                       uint64_t* bar) {
+    constexpr int d = PF::d, RS = PF::RS, RP = PF::RP, NR = PF::NR;
     const int tid = threadIdx.x, nth = blockDim.x;
-    const float* __restrict__ xb = X + b * L * d;
-
-    f2* tab = reinterpret_cast<f2*>(smem_raw);                                   // [CL][UP][RS]
-    float* raw = reinterpret_cast<float*>(smem_raw + (size_t)CL * UP * RS * 8);  // [(slen+1)*d + 4]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(raw + g.raw_floats + 4);         // staging mbarrier
-
-    auto phase = [&](int i) {
-        if (g.phases != nullptr && tid == 0) g.phases[rowid * 10 + i] = clock64();
-    };
-    phase(0);
-    pdl_trigger();  // the next launch may start on free SMs now
-    // X[b, 0, c] for the chunk starts (P_1 = X[s_j] - X[0]) and P^(0)_1, issued early
-    const bool active = tid < UP * P;
-    const int k = active ? tid / P : 0;
-    const int pre = active ? tid - (tid / P) * P : 0;
-    int dig[PF::QS];
-#pragma unroll
-    for (int q = 0; q < PF::QS; ++q) dig[q] = (Q > 0) ? (pre / ipow(d, Q > 0 ? Q - 1 - q : 0)) % d : 0;
-    float x0[Q == 0 ? d : 1];
-#pragma unroll
-    for (int c = 0; c < (Q == 0 ? d : 1); ++c) x0[c] = __ldg(xb + (Q == 0 ? c : dig[0]));
-    float p10v = 0.f;
-    if (P1S && tid < d) p10v = __ldg(xb + seg0 * d + tid) - __ldg(xb + tid);
     // 1. stage the segment's points X[seg0 .. seg0+slen]: one TMA bulk copy of
     //    the 16-byte-aligned body (completion on an mbarrier), plain loads for
     //    the <= 3 ragged floats at each end. raw is shifted so body addresses
@@ -653,7 +598,6 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
         }
     }
     __syncthreads();
-    phase(1);
     // 2. the operand table: row (s, kk) = (δ_{2kk}[c]/m, δ_{2kk+1}[c]/m), m = 1..NR.
     //    Column (kk, c) is split into `parts` contiguous step ranges, one per thread;
     //    steps where both chunks are real run predicate-free, padding steps (δ = 0,
@@ -699,6 +643,78 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
             }
         }
     }
+    return raw;
+}
+
+// Geometry of one pair-kernel launch (host and device agree on it).
+struct PairGeom {
+    int G;          // segments per path (grid = B * G)
+    int64_t SL;     // steps per segment
+    int U, UP, CL;  // chunks per segment (even), pair-units, steps per chunk
+    int threads;    // block size (multiple of 32, >= UP * P)
+    int raw_floats; // (SL + 1) * d rounded up to 4
+    long long* phases;  // optional [grid][8] SM-clock stamps of thread 0 (tools/pair_probe.py)
+    int* counters;      // G > 1: [B] arrival counters (zero between launches)
+    int smem_bytes;     // dynamic shared memory of the launch (the last 16 bytes hold a flag)
+    float* final_out;   // G > 1: (B, D) signatures (the kernel's `out` then holds the (B*G, D) segment rows)
+};
+
+template <int d, int N, int Q>
+__host__ __device__ constexpr size_t pair_smem_bytes(int U, int CL, int raw_floats, int G = 1) {
+    using PF = PairFold<d, N, Q>;
+    const size_t seg = G > 1 ? (CombineLayout<d, N>::floats(G, 0) + (size_t)G * ipow(d, N)) * 4 : 0;
+    const size_t fold = (size_t)CL * (U / 2) * PF::RS * 8 + (size_t)raw_floats * 4 + 16 + 16;
+    const size_t comb = CombineLayout<d, N>::floats(U, U / 2) * 4;
+    const size_t m = fold > comb ? fold : comb;
+    return (m > seg ? m : seg) + 16;  // + the segment-combine flag
+}
+
+// X: (B, L, d) fp32. grid = B * G CTAs; CTA (b, g) folds steps
+// [g*SL, min((g+1)*SL, M)) of path b as U chunks and writes row b*G + g of
+// `out` ((B*G, D)): A_seg ⊠ C_seg with A_seg = (1, X[seg start] - X[0], 0, ...),
+// i.e. the path's signature when G == 1.
+template <int DIM, int DEPTH, int Q, int NT, int MINB, bool P1S = (DIM > 1 && DEPTH > 1)>
+__global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict__ X, int64_t L, PairGeom g,
+                                                        float* __restrict__ out) {
+    using PF = PairFold<DIM, DEPTH, Q>;
+    using CLY = CombineLayout<DIM, DEPTH>;
+    constexpr int d = DIM, N = DEPTH, P = PF::P, RS = PF::RS, RP = PF::RP, NR = PF::NR;
+    constexpr int D = level_off(DIM, DEPTH);
+    constexpr int DL = CLY::DL, DC = CLY::DC, LN = CLY::LN, FJ = PF::FJ;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+
+    const int64_t rowid = blockIdx.x;
+    const int64_t b = rowid / g.G, sg = rowid - b * g.G;
+    const int64_t M = L - 1;
+    const int64_t seg0 = sg * g.SL < M ? sg * g.SL : M;
+    const int64_t slen = (seg0 + g.SL < M ? seg0 + g.SL : M) - seg0;
+    const int U = g.U, UP = g.UP, CL = g.CL;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const float* __restrict__ xb = X + b * L * d;
+
+    f2* tab = reinterpret_cast<f2*>(smem_raw);                                   // [CL][UP][RS]
+    float* raw = reinterpret_cast<float*>(smem_raw + (size_t)CL * UP * RS * 8);  // [(slen+1)*d + 4]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(raw + g.raw_floats + 4);         // staging mbarrier
+
+    auto phase = [&](int i) {
+        if (g.phases != nullptr && tid == 0) g.phases[rowid * 10 + i] = clock64();
+    };
+    phase(0);
+    pdl_trigger();  // the next launch may start on free SMs now
+    // X[b, 0, c] for the chunk starts (P_1 = X[s_j] - X[0]) and P^(0)_1, issued early
+    const bool active = tid < UP * P;
+    const int k = active ? tid / P : 0;
+    const int pre = active ? tid - (tid / P) * P : 0;
+    int dig[PF::QS];
+#pragma unroll
+    for (int q = 0; q < PF::QS; ++q) dig[q] = (Q > 0) ? (pre / ipow(d, Q > 0 ? Q - 1 - q : 0)) % d : 0;
+    float x0[Q == 0 ? d : 1];
+#pragma unroll
+    for (int c = 0; c < (Q == 0 ? d : 1); ++c) x0[c] = __ldg(xb + (Q == 0 ? c : dig[0]));
+    float p10v = 0.f;
+    if (P1S && tid < d) p10v = __ldg(xb + seg0 * d + tid) - __ldg(xb + tid);
+    raw = pair_stage_and_table<PF>(xb, seg0, slen, CL, UP, tab, raw, bar);
+    phase(1);
     // 3. per-thread state: slice `pre` of chunks 2k and 2k+1, started from (1, X[s_j] - X[0], 0, ...)
     f2 st[PF::S];
 #pragma unroll

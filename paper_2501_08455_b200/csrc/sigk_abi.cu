@@ -649,6 +649,116 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
     return rc;
 }
 
+// Prefix stream (reference signature_stream, kernels.cpp:156-198): out is
+// (B, L-1, D), row t = signature of X[0..t+1]. fp32 shapes with a pair
+// variant use the two-pass chunk-pair stream kernel (stream_kernel.cuh); the
+// rest use the element-parallel generic stream kernel.
+template <typename Real>
+static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* out, cudaStream_t s,
+                         const sigk_tuning* tun, sigk_stats* st) {
+    const bool is_f64 = sizeof(Real) == 8;
+    int64_t D = 0, p = 1;
+    for (int n = 0; n < N; ++n) {
+        p *= d;
+        D += p;
+    }
+    const int64_t M = L - 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    sigk_stats local{};
+    local.segments = 1;
+    local.launches = 1;
+    cudaError_t e = cudaErrorInvalidValue;
+    bool done = false;
+    if (!is_f64 && !(tun && (tun->force_generic || tun->family == SIGK_FAMILY_GENERIC))) {
+        sigk_tuning tp = tun ? *tun : sigk_tuning{};
+        tp.family = SIGK_FAMILY_PAIR;
+        tp.segments = 1;
+        const Plan plan = cached_plan(d, N, false, dev, tp.plan_rows > 0 ? tp.plan_rows : B, M, D, &tp);
+        if (plan.v && plan.v->stream_launch) {
+            const bool overlap = !(tun && tun->no_overlap) &&
+                                 may_overlap_previous(dev, s, X, sizeof(Real) * B * L * d, out, sizeof(Real) * B * M * D);
+            e = plan.v->stream_launch(X, B, L, plan.U, out, s, overlap);
+            if (e == cudaSuccess) {
+                done = true;
+                local.family = SIGK_FAMILY_PAIR;
+                local.prefix_len = plan.v->Q;
+                local.threads_per_unit = plan.v->P;
+                local.chunks = std::max(2, plan.U / 2 * 2);
+                local.fold_steps = (M + local.chunks - 1) / local.chunks;
+            } else if (e != cudaErrorInvalidValue) {
+                return cuda_fail(e, "stream launch");
+            }
+        }
+        cudaGetLastError();
+    }
+    if (!done) {
+        may_overlap_previous(dev, s, X, 0, out, sizeof(Real) * B * M * D);
+        e = is_f64 ? launch_generic_stream_f64(X, B, L, d, N, out, s) : launch_generic_stream_f32(X, B, L, d, N, out, s);
+        if (e != cudaSuccess) return cuda_fail(e, "generic stream launch");
+        local.family = SIGK_FAMILY_GENERIC;
+        local.prefix_len = -1;
+        local.chunks = 1;
+        local.fold_steps = M;
+    }
+    if (st) *st = local;
+    return SIGK_OK;
+}
+
+template <typename Real>
+static int stream_impl(const Real* X, size_t B, size_t L, int d, int N, Real* out, unsigned flags, void* stream,
+                       const sigk_tuning* tun, sigk_stats* st) {
+    g_err.clear();
+    int rc = validate(X, B, L, d, N, out);
+    if (rc != SIGK_OK) return rc;
+    if (L < 2) return fail(SIGK_EDOMAIN, "signature_stream: need at least 2 points, got L = " + std::to_string(L));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    size_t D = 0;
+    sigk_sig_dim(d, N, &D);
+    const size_t xbytes = sizeof(Real) * B * L * d, obytes = sizeof(Real) * B * (L - 1) * D;
+    const bool xdev = flags & SIGK_X_ON_DEVICE, odev = flags & SIGK_OUT_ON_DEVICE;
+    cudaError_t e;
+    if (xdev && odev) {
+        rc = stream_device<Real>(X, (int64_t)B, (int64_t)L, d, N, out, s, tun, st);
+        if (rc == SIGK_OK) {
+            e = cudaPeekAtLastError();
+            if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
+        }
+        return rc;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Staging& stg = staging_for(dev, s);
+    std::lock_guard<std::mutex> lock(stg.mu);
+    const size_t ooff = xdev ? 0 : (xbytes + 255) / 256 * 256;
+    const size_t need = ooff + (odev ? 0 : obytes);
+    if (stg.n < need) {
+        if (stg.p) cudaFree(stg.p);
+        stg.p = nullptr;
+        stg.n = 0;
+        e = cudaMalloc(&stg.p, need);
+        if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
+        stg.n = need;
+    }
+    const Real* Xd = X;
+    Real* Od = out;
+    if (!xdev) {
+        Real* xbuf = static_cast<Real*>(stg.p);
+        e = cudaMemcpyAsync(xbuf, X, xbytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+        Xd = xbuf;
+    }
+    if (!odev) Od = reinterpret_cast<Real*>(static_cast<char*>(stg.p) + ooff);
+    rc = stream_device<Real>(Xd, (int64_t)B, (int64_t)L, d, N, Od, s, tun, st);
+    if (rc == SIGK_OK && !odev) {
+        e = cudaMemcpyAsync(out, Od, obytes, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
+    }
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && rc == SIGK_OK) rc = cuda_fail(e, "stream synchronize");
+    return rc;
+}
+
 // One non-blocking stream per device for the sharded entry (created once, so
 // its staging buffers are reused across calls).
 static cudaStream_t shard_stream(int dev) {
@@ -744,6 +854,16 @@ int sigk_signature_f64(const double* X, size_t B, size_t L, int d, int N, double
     return sigk::signature_impl<double>(X, B, L, d, N, out, flags, stream, tuning, stats);
 }
 
+int sigk_signature_stream_f32(const float* X, size_t B, size_t L, int d, int N, float* out, unsigned flags,
+                              void* stream, const sigk_tuning* tuning, sigk_stats* stats) {
+    return sigk::stream_impl<float>(X, B, L, d, N, out, flags, stream, tuning, stats);
+}
+
+int sigk_signature_stream_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags,
+                              void* stream, const sigk_tuning* tuning, sigk_stats* stats) {
+    return sigk::stream_impl<double>(X, B, L, d, N, out, flags, stream, tuning, stats);
+}
+
 int sigk_signature_sharded_f32(const float* X, size_t B, size_t L, int d, int N, float* out, int num_gpus,
                                sigk_stats* stats) {
     return sigk::sharded_impl<float>(X, B, L, d, N, out, num_gpus, stats);
@@ -807,6 +927,24 @@ cudaError_t launch_generic_f32(const void* X, int64_t B, int64_t L, int d, int N
 }
 cudaError_t launch_generic_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s) {
     return gen<double>(X, B, L, d, N, out, s);
+}
+template <typename Real>
+static cudaError_t gen_stream(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s) {
+    const int64_t D = level_off(d, N);
+    if (N > kGenericMaxDepth) return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)B);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = sizeof(Real) * d;
+    cfg.stream = s;
+    return cudaLaunchKernelEx(&cfg, generic_stream_kernel<Real>, static_cast<const Real*>(X), L, d, N, D,
+                              static_cast<Real*>(out));
+}
+cudaError_t launch_generic_stream_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s) {
+    return gen_stream<float>(X, B, L, d, N, out, s);
+}
+cudaError_t launch_generic_stream_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s) {
+    return gen_stream<double>(X, B, L, d, N, out, s);
 }
 cudaError_t launch_brownian_f32(void* X, int64_t B, int64_t L, int d, uint64_t seed, int64_t row0, cudaStream_t s) {
     return brown<float>(X, B, L, d, seed, row0, s);

@@ -58,6 +58,29 @@ SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats) {
 
 }  // namespace
 
+PrefixSignatureBatch signature_stream(const PathBatch& paths, int depth, KernelKind kernel, const ExecutionCaps& caps,
+                                      KernelStats* stats) {
+    validate_paths(paths);
+    validate_depth(depth);
+    if (paths.len < 2)
+        throw DomainError("signature_stream: need at least 2 points, got L = " + std::to_string(paths.len));
+    (void)select_kernel(kernel, caps, paths.len);  // accepted for source compatibility (kernels.cpp:165)
+    PrefixSignatureBatch out;
+    out.batch = paths.batch;
+    out.prefixes = paths.len - 1;
+    out.dim = paths.dim;
+    out.depth = depth;
+    out.flat.resize(paths.batch * out.prefixes * sig_dim(paths.dim, depth));
+    sigk_stats st{};
+    check(sigk_signature_stream_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, out.flat.data(), 0u,
+                                    nullptr, nullptr, &st));
+    if (stats) {
+        stats->fold_steps = st.fold_steps;
+        stats->scan_passes = st.scan_passes;
+    }
+    return out;
+}
+
 std::vector<double> SignatureBatch::row(std::size_t b) const {
     const std::size_t w = width();
     return std::vector<double>(flat.begin() + static_cast<std::ptrdiff_t>(b * w),

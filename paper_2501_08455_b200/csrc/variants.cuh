@@ -12,6 +12,7 @@
 #include "ipair_kernel.cuh"
 #include "pair_kernel.cuh"
 #include "path_kernel.cuh"
+#include "stream_kernel.cuh"
 #include "variants.h"
 
 namespace sigk {
@@ -179,9 +180,40 @@ struct PairVariant {
         if (e != cudaSuccess) return e;
         return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kernel, threads(U), sm);
     }
+
+    // prefix stream: one CTA per path; the largest stage tile TS in {8, 4, 2, 1} that fits
+    static constexpr auto skernel = pair_stream_kernel<DIM, DEPTH, Q, NT, MINB>;
+    static std::atomic<uint64_t> ssmem_done;
+    static cudaError_t stream_launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s,
+                                     bool overlap) {
+        const int64_t M = L - 1;
+        U = std::max(2, U / 2 * 2);
+        const int CL = (int)((M + U - 1) / U);
+        int TS = 8;
+        size_t sm = 0;
+        for (; TS >= 1; TS /= 2) {
+            sm = stream_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(M), TS);
+            if (sm <= 227 * 1024) break;
+        }
+        if (TS < 1) return cudaErrorInvalidValue;
+        cudaError_t e = opt_in_smem(skernel, sm, ssmem_done);
+        if (e != cudaSuccess) return e;
+        PairGeom g{};
+        g.G = 1;
+        g.SL = M;
+        g.U = U;
+        g.UP = U / 2;
+        g.CL = CL;
+        g.threads = threads(U);
+        g.raw_floats = raw_floats(M);
+        return launch_maybe_overlapped(skernel, dim3((unsigned)B), dim3(g.threads), sm, s, overlap,
+                                       static_cast<const float*>(X), L, g, TS, static_cast<float*>(out));
+    }
 };
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::smem_done{0};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::ssmem_done{0};
 
 // Smallest Q whose pair state (two chunks) fits ~80 registers, or -1.
 constexpr int pick_q_pair(int d, int N) {
@@ -200,10 +232,11 @@ Variant make_pair_variant() {
     int chen = 0;
     for (int n = 2; n <= DEPTH; ++n) chen += (n - 2) * ipow(DIM, n);
     Variant v{DIM, DEPTH, Q, PF::P, PF::ops_per_step(), PF::loads_per_step(), chen, KernelFamily::Pair, V::NT, 0,
-              nullptr, nullptr};
+              nullptr, nullptr, nullptr, nullptr, 0, nullptr};
     v.pair_launch = &V::launch;
     v.pair_occupancy = &V::occupancy;
     v.pair_units_max = V::NT / PF::P;
+    v.stream_launch = &V::stream_launch;
     return v;
 }
 
@@ -255,7 +288,7 @@ Variant make_ipair_variant() {
     using V = IPairVariant<DIM, DEPTH, Q>;
     using F = typename V::F;
     Variant v{DIM, DEPTH, Q, F::P, F::pipe_cycles(), 0, 0, KernelFamily::PFlat, V::NT, V::T,
-              &V::launch, &V::occupancy, nullptr, nullptr, 0};
+              &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr};
     return v;
 }
 
@@ -268,11 +301,11 @@ Variant make_variant() {
     if constexpr (SF::P > 256) {
         using V = FlatVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Flat, V::NT, V::T,
-                       &V::launch, &V::occupancy, nullptr, nullptr, 0};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr};
     } else {
         using V = PathVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Path, V::NTMAX, V::T,
-                       &V::launch, &V::occupancy, nullptr, nullptr, 0};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr};
     }
 }
 

@@ -49,12 +49,16 @@ struct Variant {
     cudaError_t (*pair_launch)(const PairLaunch& a);
     cudaError_t (*pair_occupancy)(int U, int CL, int64_t SL, int G, int* blocks_per_sm);  // 0: does not fit
     int pair_units_max;  // max U/2 per CTA
+    // pair family: prefix stream (B, L-1, D) of whole paths; cudaErrorInvalidValue when L does not fit one CTA
+    cudaError_t (*stream_launch)(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, bool overlap);
 };
 
 const Variant* find_variant(int d, int N, bool is_f64);  // first (smallest-Q) candidate
 int find_variants(int d, int N, bool is_f64, const Variant** out, int max);
 cudaError_t launch_generic_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
 cudaError_t launch_generic_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
+cudaError_t launch_generic_stream_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
+cudaError_t launch_generic_stream_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
 cudaError_t launch_brownian_f32(void* X, int64_t B, int64_t L, int d, uint64_t seed, int64_t row0, cudaStream_t s);
 cudaError_t launch_brownian_f64(void* X, int64_t B, int64_t L, int d, uint64_t seed, int64_t row0, cudaStream_t s);
 

@@ -1,2 +1,1 @@
-for c in c2 c3 c4 c5 c1; do timeout 300 python bench.py --config $c --no-cpu --e2e-steps 50 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
-timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.txt 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:pair_stream -s 2 -c 1 -o gpurun_out/stream_c2 python tools/stream_bench.py 128 1000 5 4 3 > gpurun_out/ncu_stream.log 2>&1
