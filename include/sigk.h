@@ -137,6 +137,10 @@ int sigk_signature_sharded_f64(const double* X, size_t B, size_t L, int d, int N
 int sigk_brownian_f32(float* X_dev, size_t B, size_t L, int d, uint64_t seed, size_t row0, void* stream);
 int sigk_brownian_f64(double* X_dev, size_t B, size_t L, int d, uint64_t seed, size_t row0, void* stream);
 
+/* The reference's benchmark inputs (bench.cpp:134-161): (B, L, d) float64
+ * random walks from (seed, B, L, d), bit-identical to make_bench_paths. */
+int sigk_make_bench_paths(uint64_t seed, size_t B, size_t L, int d, double* out);
+
 /* 1 when a register-sliced fast variant exists for (d, N) in this precision
  * (0: the shape-generic kernel is used). *Q receives the prefix length. */
 int sigk_has_fast_variant(int d, int N, int is_f64, int* Q);

@@ -35,12 +35,15 @@ def _units():
             units.append((f"variants_{real}_d{d}", os.path.join(CSRC, "variants_inst.cu"),
                           [f"-DSIGK_REAL={real}", f"-DSIGK_DIM={d}"]))
     units.append(("sigkit_api", os.path.join(CSRC, "sigkit_api.cpp"), []))
+    units.append(("bench_api", os.path.join(CSRC, "bench_api.cpp"), []))
     return units
 
 
 def _stamp(src: str, extra: list[str]) -> str:
     h = hashlib.sha1()
-    for p in [src] + [os.path.join(CSRC, x) for x in HEADERS] + [os.path.join(ROOT, "include", "sigk.h")]:
+    incs = [os.path.join(ROOT, "include", "sigk.h")] + [os.path.join(ROOT, "include", "sigkit", x)
+                                                         for x in sorted(os.listdir(os.path.join(ROOT, "include", "sigkit")))]
+    for p in [src] + [os.path.join(CSRC, x) for x in HEADERS] + incs:
         with open(p, "rb") as f:
             h.update(f.read())
     h.update(" ".join(NVFLAGS + ARCH + extra).encode())
@@ -85,7 +88,25 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    _build_cli(verbose)
     return LIB
+
+
+def _build_cli(verbose: bool = False) -> None:
+    """tools/sigbench: the reference sigbench CLI over the B200 library."""
+    src = os.path.join(ROOT, "tools", "sigbench.cpp")
+    exe = os.path.join(ROOT, "tools", "sigbench")
+    if not os.path.exists(src):
+        return
+    if os.path.exists(exe) and os.path.getmtime(exe) >= max(os.path.getmtime(src), os.path.getmtime(LIB)):
+        return
+    cmd = ["g++", "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", exe, LIB,
+           "-Wl,-rpath,$ORIGIN/../paper_2501_08455_b200"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"sigbench build failed: {' '.join(cmd)}\n{r.stderr}")
+    if verbose:
+        print("  built  tools/sigbench")
 
 
 if __name__ == "__main__":

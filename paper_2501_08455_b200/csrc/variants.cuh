@@ -356,9 +356,9 @@ struct DimTable {
 // translation unit (variants_inst.cu) so the build parallelises.
 #define SIGK_DEPTHS_1 1, 2, 3, 4, 5, 6
 #define SIGK_DEPTHS_2 1, 2, 3, 4, 5, 6
-#define SIGK_DEPTHS_3 1, 2, 3, 4, 5
-#define SIGK_DEPTHS_4 1, 2, 3, 4, 5
-#define SIGK_DEPTHS_5 1, 2, 3, 4, 5
+#define SIGK_DEPTHS_3 1, 2, 3, 4, 5, 6
+#define SIGK_DEPTHS_4 1, 2, 3, 4, 5, 6
+#define SIGK_DEPTHS_5 1, 2, 3, 4, 5, 6
 #define SIGK_DEPTHS_6 1, 2, 3, 4
 #define SIGK_DEPTHS_7 1, 2, 3, 4
 #define SIGK_DEPTHS_8 1, 2, 3, 4

@@ -83,3 +83,31 @@ def test_kernel_names_and_dispatch(sk):
     assert sk.select_kernel(K.Auto, accel, 63) is K.Sequential
     assert sk.select_kernel(K.Auto, plain, 1000) is K.Sequential
     assert sk.select_kernel(K.Parallel, plain, 2) is K.Parallel
+
+
+def test_make_bench_paths_matches_reference(sk):
+    # the reference's own generator (bench.cpp:134-161) compiled from its sources
+    import ctypes as C
+
+    from oracle import oracle as O
+
+    if O.ref() is None:
+        pytest.skip("oracle/_ref (the compiled reference) is not built")
+    lib = sk.lib()
+    lib.sigk_make_bench_paths.argtypes = [C.c_uint64, C.c_size_t, C.c_size_t, C.c_int, C.c_void_p]
+    for seed, B, L, d in ((42, 3, 50, 2), (7, 2, 1, 3), (123456789, 4, 17, 5)):
+        got = np.empty((B, L, d))
+        assert lib.sigk_make_bench_paths(seed, B, L, d, got.ctypes.data) == 0
+        assert np.array_equal(got, O.ref_make_bench_paths(seed, B, L, d))
+
+
+def test_sigbench_cli_rejects_bad_flags():
+    import subprocess
+
+    exe = os.path.join(ROOT, "tools", "sigbench")
+    if not os.path.exists(exe):
+        pytest.skip("tools/sigbench not built")
+    r = subprocess.run([exe, "--dims", "0"], capture_output=True, text=True)
+    assert r.returncode == 1 and "--dims entries must be positive" in r.stderr
+    r = subprocess.run([exe, "--dtype", "f16"], capture_output=True, text=True)
+    assert r.returncode == 1

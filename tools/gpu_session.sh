@@ -1,1 +1,3 @@
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:pair_stream -s 2 -c 1 -o gpurun_out/stream_c2 python tools/stream_bench.py 128 1000 5 4 3 > gpurun_out/ncu_stream.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1
+./tools/sigbench --paper-grid --dims 5 --dtype f32 --kernels sequential > gpurun_out/sigbench_paper_f32.csv 2> gpurun_out/sigbench.err
+./tools/sigbench --paper-grid --dims 5 --dtype f64 --kernels sequential > gpurun_out/sigbench_paper_f64.csv 2>> gpurun_out/sigbench.err
