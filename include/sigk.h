@@ -16,6 +16,9 @@
  *                         ← sigkit::signature_stream  include/sigkit/kernels.hpp:110-114,
  *                           src/kernels.cpp:156-198 (every prefix signature, (B, L-1, D);
  *                           row t = signature of X[0..t+1]; L < 2 is a DomainError)
+ *   sigk_signature_vjp_f32/_f64
+ *                         ← sigkit::signature_vjp  include/sigkit/autodiff.hpp:35-38,
+ *                           src/autodiff.cpp:31-107, 218-224 (reverse mode)
  *   sigk_signature_sharded_f32/_f64
  *                         ← signature() over a batch split across GPUs (rows are independent,
  *                           SPEC.md:220-221; tests/test_kernels.cpp:252-263)
@@ -122,6 +125,14 @@ int sigk_signature_stream_f32(const float* X, size_t B, size_t L, int d, int N, 
                               void* stream, const sigk_tuning* tuning, sigk_stats* stats);
 int sigk_signature_stream_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags,
                               void* stream, const sigk_tuning* tuning, sigk_stats* stats);
+
+/* Reverse mode: grad (B, L, d) = d<cotangent, Sig(X)>/dX for cotangent (B, D).
+ * flags: SIGK_X_ON_DEVICE means X, cotangent and grad are all device buffers
+ * (asynchronous on `stream`); otherwise all three are host buffers. */
+int sigk_signature_vjp_f32(const float* X, size_t B, size_t L, int d, int N, const float* cotangent, float* grad,
+                           unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats);
+int sigk_signature_vjp_f64(const double* X, size_t B, size_t L, int d, int N, const double* cotangent, double* grad,
+                           unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats);
 
 /* Host buffers in and out; rows [g*ceil(B/G), ...) run on device g, one host
  * thread per device, each shard copied in, folded and copied back into its

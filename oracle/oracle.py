@@ -92,6 +92,8 @@ def ref():
             lib.ref_restricted_exp.argtypes = [C.c_int, C.c_int, _dp, _dp]
             lib.ref_make_bench_paths.argtypes = [C.c_uint64, _sz, _sz, C.c_int, _dp]
             lib.ref_random_paths.argtypes = [C.c_uint64, _sz, _sz, C.c_int, C.c_double, _dp]
+            lib.ref_signature_vjp.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp, C.c_int, _dp]
+            lib.ref_finite_diff_grad.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp, C.c_double, _dp]
             _ref = lib
     return _ref
 
@@ -226,3 +228,23 @@ def ref_make_bench_paths(seed: int, B: int, L: int, d: int) -> np.ndarray:
     out = np.empty((B, L, d), np.float64)
     _ref_call(ref().ref_make_bench_paths(seed, B, L, d, _ptr(out, _dp)))
     return out
+
+
+def ref_vjp(X: np.ndarray, N: int, cot: np.ndarray, kernel: str = "sequential") -> np.ndarray:
+    """The reference's signature_vjp (autodiff.cpp:218-224) on (B, L, d) float64."""
+    X = np.ascontiguousarray(X, np.float64)
+    cot = np.ascontiguousarray(cot, np.float64)
+    B, L, d = X.shape
+    g = np.empty_like(X)
+    _ref_call(ref().ref_signature_vjp(_ptr(X, _dp), B, L, d, N, _ptr(cot, _dp), 1 if kernel == "parallel" else 0,
+                                      _ptr(g, _dp)))
+    return g
+
+
+def ref_finite_diff(X: np.ndarray, N: int, cot: np.ndarray, h: float = 1e-5) -> np.ndarray:
+    X = np.ascontiguousarray(X, np.float64)
+    cot = np.ascontiguousarray(cot, np.float64)
+    B, L, d = X.shape
+    g = np.empty_like(X)
+    _ref_call(ref().ref_finite_diff_grad(_ptr(X, _dp), B, L, d, N, _ptr(cot, _dp), h, _ptr(g, _dp)))
+    return g

@@ -18,6 +18,7 @@
 #include <thread>
 #include <vector>
 
+#include "sigkit/autodiff.hpp"
 #include "helpers.hpp"  // testutil::random_paths (reference tests/helpers.hpp:16-36)
 #include "sigkit/bench.hpp"
 #include "sigkit/detail/sig_core.hpp"
@@ -176,6 +177,36 @@ int ref_random_paths(std::uint64_t seed, std::size_t B, std::size_t L, int d, do
     return guarded([&] {
         auto p = testutil::random_paths(seed, B, L, d, step_scale);
         std::memcpy(out, p.values.data(), p.values.size() * sizeof(double));
+    });
+}
+
+// signature_vjp (autodiff.cpp:218-224): kernel 0 = sequential (fold adjoint,
+// :31-107), 1 = parallel (scan adjoint, :114-214).
+int ref_signature_vjp(const double* x, std::size_t B, std::size_t L, int d, int N, const double* cot, int kernel,
+                      double* grad) {
+    return guarded([&] {
+        sigkit::SignatureCotangent c;
+        c.batch = B;
+        c.dim = d;
+        c.depth = N;
+        c.values.assign(cot, cot + B * sigkit::sig_dim(d, N));
+        auto g = sigkit::signature_vjp(make_batch(x, B, L, d), N, c,
+                                       kernel == 1 ? sigkit::KernelKind::Parallel : sigkit::KernelKind::Sequential);
+        std::memcpy(grad, g.values.data(), g.values.size() * sizeof(double));
+    });
+}
+
+// finite_diff_grad (autodiff.cpp:226-266): central differences, step h.
+int ref_finite_diff_grad(const double* x, std::size_t B, std::size_t L, int d, int N, const double* cot, double h,
+                         double* grad) {
+    return guarded([&] {
+        sigkit::SignatureCotangent c;
+        c.batch = B;
+        c.dim = d;
+        c.depth = N;
+        c.values.assign(cot, cot + B * sigkit::sig_dim(d, N));
+        auto g = sigkit::finite_diff_grad(make_batch(x, B, L, d), N, c, h);
+        std::memcpy(grad, g.values.data(), g.values.size() * sizeof(double));
     });
 }
 

@@ -127,6 +127,9 @@ def lib():
         for n in ("sigk_signature_stream_f32", "sigk_signature_stream_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, C.c_uint, vp, C.POINTER(_Tuning),
                                       C.POINTER(_Stats)]
+        for n in ("sigk_signature_vjp_f32", "sigk_signature_vjp_f64"):
+            getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, vp, C.c_uint, vp, C.POINTER(_Tuning),
+                                      C.POINTER(_Stats)]
         for n in ("sigk_signature_sharded_f32", "sigk_signature_sharded_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, C.c_int, C.POINTER(_Stats)]
         for n in ("sigk_brownian_f32", "sigk_brownian_f64"):
@@ -296,6 +299,44 @@ def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, ca
     return out
 
 
+def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.Auto,
+                  caps: ExecutionCaps | None = None, stats: KernelStats | None = None):
+    """Reference ``sigkit::signature_vjp`` (autodiff.cpp:218-224): d<cotangent, Sig(X)>/dX,
+    (B, L, d), for a (B, D) cotangent. numpy in -> numpy out; CUDA tensors in -> CUDA tensor out."""
+    select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
+    st = _Stats()
+    if _is_torch(paths):
+        import torch
+
+        B, L, d = _validate_shape(paths.shape, depth)
+        X = paths.contiguous()
+        cot = cotangent.to(device=X.device, dtype=X.dtype).contiguous()
+        if tuple(cot.shape) != (B, sig_dim(d, depth)):
+            raise DomainError("signature_vjp: cotangent shape does not match paths/depth")
+        grad = torch.empty_like(X)
+        fn = lib().sigk_signature_vjp_f32 if X.dtype == torch.float32 else lib().sigk_signature_vjp_f64
+        with torch.cuda.device(X.device):
+            s = torch.cuda.current_stream(X.device).cuda_stream
+            _check(fn(X.data_ptr(), B, L, d, depth, cot.data_ptr(), grad.data_ptr(), SIGK_X_ON_DEVICE, s, None,
+                      C.byref(st)))
+    else:
+        X = np.asarray(paths)
+        B, L, d = _validate_shape(X.shape, depth)
+        if X.dtype not in (np.float32, np.float64):
+            X = X.astype(np.float64)
+        X = np.ascontiguousarray(X)
+        cot = np.ascontiguousarray(cotangent, dtype=X.dtype)
+        if cot.shape != (B, sig_dim(d, depth)):
+            raise DomainError("signature_vjp: cotangent shape does not match paths/depth")
+        grad = np.empty_like(X)
+        fn = lib().sigk_signature_vjp_f32 if X.dtype == np.float32 else lib().sigk_signature_vjp_f64
+        _check(fn(X.ctypes.data, B, L, d, depth, cot.ctypes.data, grad.ctypes.data, 0, None, None, C.byref(st)))
+    if stats is not None:
+        for f, _ in _Stats._fields_:
+            setattr(stats, f, getattr(st, f))
+    return grad
+
+
 def signature_sequential(paths, depth: int, stats: KernelStats | None = None, **kw):
     """Reference ``signature_sequential`` (kernels.cpp:106-122)."""
     return _run(paths, depth, stats, **kw)
@@ -347,7 +388,7 @@ __all__ = [
     "DomainError", "ResourceError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
-    "signature_stream",
+    "signature_stream", "signature_vjp",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
     "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES",
 ]

@@ -17,6 +17,7 @@
 #include "../../include/sigk.h"
 #include "generic.cuh"
 #include "variants.h"
+#include "vjp_kernel.cuh"
 
 namespace sigk {
 
@@ -759,6 +760,113 @@ static int stream_impl(const Real* X, size_t B, size_t L, int d, int N, Real* ou
     return rc;
 }
 
+// Reverse mode (reference signature_vjp, autodiff.cpp:218-224): the prefix
+// states come from the stream kernels into stream-ordered scratch, then
+// vjp_kernel walks the steps backwards (vjp_kernel.cuh).
+template <typename Real>
+static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const Real* cot, Real* grad, cudaStream_t s,
+                      const sigk_tuning* tun, sigk_stats* st) {
+    int64_t D = 0, p = 1;
+    for (int n = 0; n < N; ++n) {
+        p *= d;
+        D += p;
+    }
+    const int64_t M = L - 1;
+    cudaError_t e;
+    Real* states = nullptr;
+    if (M > 0) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&states), sizeof(Real) * B * M * D, s);
+        if (e != cudaSuccess) return cuda_fail(e, "vjp state allocation");
+        const int rc = stream_device<Real>(X, B, L, d, N, states, s, tun, st);
+        if (rc != SIGK_OK) {
+            cudaFreeAsync(states, s);
+            return rc;
+        }
+    }
+    const size_t work = sizeof(Real) * vjp_work_elems(D, d);
+    const int use_smem = work <= 160 * 1024;
+    Real* gwork = nullptr;
+    if (!use_smem) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&gwork), work * B, s);
+        if (e != cudaSuccess) {
+            if (states) cudaFreeAsync(states, s);
+            return cuda_fail(e, "vjp work allocation");
+        }
+    } else if (work > 48 * 1024) {
+        cudaFuncSetAttribute(vjp_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)work);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)B);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = use_smem ? work : 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;  // the kernel waits for its predecessor (the states) before reading anything
+    e = cudaLaunchKernelEx(&cfg, vjp_kernel<Real>, X, L, d, N, D, static_cast<const Real*>(states), cot, grad, gwork,
+                           use_smem);
+    if (states) cudaFreeAsync(states, s);
+    if (gwork) cudaFreeAsync(gwork, s);
+    if (e != cudaSuccess) return cuda_fail(e, "vjp launch");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    may_overlap_previous(dev, s, X, 0, grad, sizeof(Real) * B * L * d);
+    if (st) st->launches += 1;
+    return SIGK_OK;
+}
+
+template <typename Real>
+static int vjp_impl(const Real* X, size_t B, size_t L, int d, int N, const Real* cot, Real* grad, unsigned flags,
+                    void* stream, const sigk_tuning* tun, sigk_stats* st) {
+    g_err.clear();
+    int rc = validate(X, B, L, d, N, grad);
+    if (rc != SIGK_OK) return rc;
+    if (cot == nullptr) return fail(SIGK_EDOMAIN, "signature_vjp: cotangent pointer is null");
+    if (N > kGenericMaxDepth) return fail(SIGK_ERESOURCE, "signature_vjp: depth above 16 is not supported");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    size_t D = 0;
+    sigk_sig_dim(d, N, &D);
+    const size_t xbytes = sizeof(Real) * B * L * d, cbytes = sizeof(Real) * B * D;
+    cudaError_t e;
+    if (flags & SIGK_X_ON_DEVICE) {
+        rc = vjp_device<Real>(X, (int64_t)B, (int64_t)L, d, N, cot, grad, s, tun, st);
+        if (rc == SIGK_OK) {
+            e = cudaPeekAtLastError();
+            if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
+        }
+        return rc;
+    }
+    // host buffers: X, cotangent in, gradient out (synchronous)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Staging& stg = staging_for(dev, s);
+    std::lock_guard<std::mutex> lock(stg.mu);
+    const size_t coff = (xbytes + 255) / 256 * 256, goff = coff + (cbytes + 255) / 256 * 256;
+    const size_t need = goff + xbytes;
+    if (stg.n < need) {
+        if (stg.p) cudaFree(stg.p);
+        stg.p = nullptr;
+        stg.n = 0;
+        e = cudaMalloc(&stg.p, need);
+        if (e != cudaSuccess) return cuda_fail(e, "staging allocation");
+        stg.n = need;
+    }
+    char* base = static_cast<char*>(stg.p);
+    Real* xd = reinterpret_cast<Real*>(base);
+    Real* cd = reinterpret_cast<Real*>(base + coff);
+    Real* gd = reinterpret_cast<Real*>(base + goff);
+    if ((e = cudaMemcpyAsync(xd, X, xbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D");
+    if ((e = cudaMemcpyAsync(cd, cot, cbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D");
+    rc = vjp_device<Real>(xd, (int64_t)B, (int64_t)L, d, N, cd, gd, s, tun, st);
+    if (rc == SIGK_OK && (e = cudaMemcpyAsync(grad, gd, xbytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        rc = cuda_fail(e, "D2H");
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && rc == SIGK_OK) rc = cuda_fail(e, "stream synchronize");
+    return rc;
+}
+
 // One non-blocking stream per device for the sharded entry (created once, so
 // its staging buffers are reused across calls).
 static cudaStream_t shard_stream(int dev) {
@@ -862,6 +970,16 @@ int sigk_signature_stream_f32(const float* X, size_t B, size_t L, int d, int N, 
 int sigk_signature_stream_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags,
                               void* stream, const sigk_tuning* tuning, sigk_stats* stats) {
     return sigk::stream_impl<double>(X, B, L, d, N, out, flags, stream, tuning, stats);
+}
+
+int sigk_signature_vjp_f32(const float* X, size_t B, size_t L, int d, int N, const float* cotangent, float* grad,
+                           unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats) {
+    return sigk::vjp_impl<float>(X, B, L, d, N, cotangent, grad, flags, stream, tuning, stats);
+}
+
+int sigk_signature_vjp_f64(const double* X, size_t B, size_t L, int d, int N, const double* cotangent, double* grad,
+                           unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats) {
+    return sigk::vjp_impl<double>(X, B, L, d, N, cotangent, grad, flags, stream, tuning, stats);
 }
 
 int sigk_signature_sharded_f32(const float* X, size_t B, size_t L, int d, int N, float* out, int num_gpus,

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "sigk.h"
+#include "sigkit/autodiff.hpp"
 #include "sigkit/kernels.hpp"
 #include "sigkit/tensor_algebra.hpp"
 
@@ -57,6 +58,64 @@ SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats) {
 }
 
 }  // namespace
+
+PathGradient signature_vjp(const PathBatch& paths, int depth, const SignatureCotangent& cot, KernelKind kernel,
+                           const ExecutionCaps& caps) {
+    // same checks and messages as the reference (autodiff.cpp:12-26)
+    if (paths.batch < 1 || paths.len < 1 || paths.dim < 1)
+        throw DomainError("signature_vjp: batch, len and dim must all be >= 1");
+    if (depth < 1) throw DomainError("signature_vjp: depth must be >= 1");
+    if (cot.batch != paths.batch || cot.dim != paths.dim || cot.depth != depth)
+        throw DomainError("signature_vjp: cotangent shape does not match paths/depth");
+    const std::size_t width = sig_dim(paths.dim, depth);
+    if (cot.values.size() != cot.batch * width)
+        throw DomainError("signature_vjp: cotangent has " + std::to_string(cot.values.size()) + " values, expected " +
+                          std::to_string(cot.batch * width));
+    validate_paths(paths);
+    (void)select_kernel(kernel, caps, paths.len);
+    PathGradient g;
+    g.batch = paths.batch;
+    g.len = paths.len;
+    g.dim = paths.dim;
+    g.values.assign(paths.values.size(), 0.0);
+    check(sigk_signature_vjp_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, cot.values.data(),
+                                 g.values.data(), 0u, nullptr, nullptr, nullptr));
+    return g;
+}
+
+PathGradient finite_diff_grad(const PathBatch& paths, int depth, const SignatureCotangent& cot, double h) {
+    PathGradient g;
+    g.batch = paths.batch;
+    g.len = paths.len;
+    g.dim = paths.dim;
+    g.values.assign(paths.values.size(), 0.0);
+    PathBatch p = paths;
+    const std::size_t width = sig_dim(paths.dim, depth);
+    auto objective = [&](std::size_t b) {
+        PathBatch one;
+        one.batch = 1;
+        one.len = p.len;
+        one.dim = p.dim;
+        one.values.assign(p.values.begin() + static_cast<std::ptrdiff_t>(b * p.len * p.dim),
+                          p.values.begin() + static_cast<std::ptrdiff_t>((b + 1) * p.len * p.dim));
+        const SignatureBatch s = signature(one, depth);
+        double acc = 0.0;
+        for (std::size_t i = 0; i < width; ++i) acc += cot.values[b * width + i] * s.flat[i];
+        return acc;
+    };
+    for (std::size_t b = 0; b < p.batch; ++b)
+        for (std::size_t i = 0; i < p.len * static_cast<std::size_t>(p.dim); ++i) {
+            double& x = p.values[b * p.len * p.dim + i];
+            const double x0 = x;
+            x = x0 + h;
+            const double fp = objective(b);
+            x = x0 - h;
+            const double fm = objective(b);
+            x = x0;
+            g.values[b * p.len * p.dim + i] = (fp - fm) / (2.0 * h);
+        }
+    return g;
+}
 
 PrefixSignatureBatch signature_stream(const PathBatch& paths, int depth, KernelKind kernel, const ExecutionCaps& caps,
                                       KernelStats* stats) {

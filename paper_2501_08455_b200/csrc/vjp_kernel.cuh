@@ -1,0 +1,211 @@
+// Reverse mode: gradient of <cotangent, Sig(X)> with respect to every path
+// point (reference signature_vjp, /root/reference/proj/src/autodiff.cpp:218-224;
+// the fold adjoint vjp_sequential :31-107).
+//
+// The forward states (every prefix signature) come from the prefix-stream
+// kernels; one CTA per path then walks the steps backwards, element-parallel
+// over the D coefficients, with exactly the reference's adjoint of
+// C = A ⊠ exp(δ):
+//     Ā_i[I]  = C̄_i[I] + Σ_j Σ_J C̄_{i+j}[I J] E_j[J]            (A = state before)
+//     Ē_j[J]  = C̄_j[J] + Σ_i Σ_I C̄_{i+j}[I J] A_i[I]            (E = exp(δ))
+// then through e_n = e_{n-1} ⊗ δ / n from the top degree down, and
+// ∂L/∂X_t = δ̄_{t-1} − δ̄_t. Reductions over a leading index (the δ̄ terms)
+// are warp shuffles in a fixed order: deterministic.
+#pragma once
+
+#include "generic.cuh"
+
+namespace sigk {
+
+template <typename Real>
+__device__ __forceinline__ Real warp_sum(Real v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// X (B, L, d); states (B, L-1, D) = prefix signatures (row t after step t);
+// cot (B, D); grad (B, L, d). work: per-CTA scratch of vjp_work_elems(D, d)
+// Reals (shared memory when it fits, else `gwork` + blockIdx * that). The
+// state row of the next step is prefetched with cp.async into a second
+// buffer while the current step computes.
+__host__ __device__ constexpr int64_t vjp_work_elems(int64_t D, int d) { return 6 * D + 3 * d + 4; }
+
+template <typename Real>
+__device__ __forceinline__ void prefetch_row(Real* dst, const Real* src, int64_t n) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        if constexpr (sizeof(Real) == 8)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst + i))),
+                         "l"(src + i)
+                         : "memory");
+        else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst + i))),
+                         "l"(src + i)
+                         : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <typename Real>
+__global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, int64_t L, int d, int N, int64_t D,
+                                                  const Real* __restrict__ states, const Real* __restrict__ cot,
+                                                  Real* __restrict__ grad, Real* __restrict__ gwork, int use_smem) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int64_t off[kGenericMaxDepth + 1];
+    __shared__ Real invfact[kGenericMaxDepth + 1];
+    const int64_t b = blockIdx.x;
+    const int64_t M = L - 1;
+    const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
+    Real* work = use_smem ? reinterpret_cast<Real*>(smem_raw) : gwork + b * vjp_work_elems(D, d);
+    Real* cbar = work;            // [D] cotangent of the state after the step
+    Real* abar = cbar + D;        // [D] ... of the state before it
+    Real* ebar = abar + D;        // [D] ... of exp(δ)
+    Real* E = ebar + D;           // [D] exp(δ)
+    Real* Ab[2] = {E + D, E + 2 * D};  // [2][D] state rows (current, next)
+    Real* dl = E + 3 * D;         // [d] δ
+    Real* db = dl + d;            // [d] δ̄ of this step
+    Real* dbn = db + d;           // [d] δ̄ of the next step
+    if (tid == 0) {
+        off[0] = 0;
+        int64_t p = 1;
+        Real f = 1;
+        invfact[0] = 1;
+        for (int n = 1; n <= N; ++n) {
+            p *= d;
+            off[n] = off[n - 1] + p;
+            f *= Real(n);
+            invfact[n] = Real(1) / f;
+        }
+    }
+    pdl_trigger();
+    pdl_wait();
+    const Real* xb = X + b * L * d;
+    const Real* sb = states + b * M * D;
+    Real* gb = grad + b * L * d;
+    for (int64_t i = tid; i < D; i += nth) cbar[i] = cot[b * D + i];
+    for (int c = tid; c < d; c += nth) dbn[c] = Real(0);
+    if (M == 0)
+        for (int c = tid; c < d; c += nth) gb[c] = Real(0);
+    const bool async_rows = use_smem;
+    if (async_rows && M >= 2) prefetch_row(Ab[(M - 1) & 1], sb + (M - 2) * D, D);
+    __syncthreads();
+    for (int64_t s = M - 1; s >= 0; --s) {
+        // state before step s (null: identity); the row for step s-1 streams in meanwhile
+        const Real* A = nullptr;
+        if (s > 0) {
+            if (async_rows) {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                A = Ab[s & 1];
+                if (s >= 2) prefetch_row(Ab[(s - 1) & 1], sb + (s - 2) * D, D);
+            } else {
+                A = sb + (s - 1) * D;
+            }
+        }
+        for (int c = tid; c < d; c += nth) {
+            dl[c] = xb[(s + 1) * d + c] - xb[s * d + c];
+            db[c] = Real(0);
+        }
+        __syncthreads();
+        // E_n[P d + c] = E_{n-1}[P] δ[c] / n, levels ascending
+        for (int n = 1; n <= N; ++n) {
+            const int psz = n == 1 ? 1 : (int)(off[n - 1] - off[n - 2]);  // d^(n-1)
+            const Real inv = Real(1) / Real(n);
+            for (int P = tid; P < psz; P += nth) {
+                const Real e = (n == 1 ? Real(1) : E[off[n - 2] + P]) * inv;
+                Real* dst = E + off[n - 1] + (int64_t)P * d;
+                for (int c = 0; c < d; ++c) dst[c] = e * dl[c];
+            }
+            __syncthreads();
+        }
+        // Ā_n[I] = C̄_n[I] + Σ_j Σ_J C̄_{n+j}[I J] E_j[J],  Ē_n[J] = C̄_n[J] + Σ_i Σ_I C̄_{i+n}[I J] A_i[I]
+        // (level by level; long dot products by a whole warp, short ones by a thread)
+        for (int n = 1; n <= N; ++n) {
+            const int sz = (int)(off[n] - off[n - 1]);
+            const int on = (int)off[n - 1];
+            const int len = (int)(off[N - n] - 0);  // Σ_{j=1}^{N-n} d^j
+            if (A == nullptr || n == N) {
+                for (int i = tid; i < sz; i += nth) {
+                    abar[on + i] = cbar[on + i];
+                    ebar[on + i] = cbar[on + i];
+                }
+            } else if (len >= 64) {
+                for (int item = warp; item < 2 * sz; item += nw) {
+                    const bool is_a = item < sz;
+                    const int I = is_a ? item : item - sz;
+                    Real acc = Real(0);
+                    if (is_a) {
+                        int w = 1;
+                        for (int j = 1; n + j <= N; ++j) {
+                            w *= d;
+                            const Real* cr = cbar + off[n + j - 1] + (int64_t)I * w;
+                            const Real* er = E + off[j - 1];
+                            for (int J = lane; J < w; J += 32) acc = fma(cr[J], er[J], acc);
+                        }
+                    } else {
+                        for (int i = 1; i + n <= N; ++i) {
+                            const int wi = (int)(off[i] - off[i - 1]);
+                            const Real* cr = cbar + off[i + n - 1] + I;
+                            const Real* ar = A + off[i - 1];
+                            for (int P = lane; P < wi; P += 32) acc = fma(cr[(int64_t)P * sz], ar[P], acc);
+                        }
+                    }
+                    acc = warp_sum(acc);
+                    if (lane == 0) (is_a ? abar : ebar)[on + I] = cbar[on + I] + acc;
+                }
+            } else {
+                for (int item = tid; item < 2 * sz; item += nth) {
+                    const bool is_a = item < sz;
+                    const int I = is_a ? item : item - sz;
+                    Real acc = cbar[on + I];
+                    if (is_a) {
+                        int w = 1;
+                        for (int j = 1; n + j <= N; ++j) {
+                            w *= d;
+                            const Real* cr = cbar + off[n + j - 1] + (int64_t)I * w;
+                            const Real* er = E + off[j - 1];
+                            for (int J = 0; J < w; ++J) acc = fma(cr[J], er[J], acc);
+                        }
+                    } else {
+                        for (int i = 1; i + n <= N; ++i) {
+                            const int wi = (int)(off[i] - off[i - 1]);
+                            const Real* cr = cbar + off[i + n - 1] + I;
+                            const Real* ar = A + off[i - 1];
+                            for (int P = 0; P < wi; ++P) acc = fma(cr[(int64_t)P * sz], ar[P], acc);
+                        }
+                    }
+                    (is_a ? abar : ebar)[on + I] = acc;
+                }
+            }
+        }
+        __syncthreads();
+        // e_n = e_{n-1} ⊗ δ / n, top degree down (autodiff.cpp:86-98)
+        for (int n = N; n >= 2; --n) {
+            const int psz = (int)(off[n - 1] - off[n - 2]);
+            const Real inv = Real(1) / Real(n);
+            const Real* en = ebar + off[n - 1];
+            for (int P = tid; P < psz; P += nth) {
+                Real acc = Real(0);
+                for (int c = 0; c < d; ++c) acc = fma(en[P * d + c], dl[c], acc);
+                ebar[off[n - 2] + P] = fma(acc, inv, ebar[off[n - 2] + P]);
+            }
+            for (int c = warp; c < d; c += nw) {
+                Real acc = Real(0);
+                for (int P = lane; P < psz; P += 32) acc = fma(en[P * d + c], E[off[n - 2] + P], acc);
+                acc = warp_sum(acc);
+                if (lane == 0) db[c] = fma(acc, inv, db[c]);
+            }
+            __syncthreads();
+        }
+        for (int c = tid; c < d; c += nth) {
+            const Real v = db[c] + ebar[c];
+            gb[(s + 1) * d + c] = v - dbn[c];
+            if (s == 0) gb[c] = -v;
+            dbn[c] = v;
+        }
+        Real* t = cbar;
+        cbar = abar;
+        abar = t;
+        __syncthreads();
+    }
+}
+
+}  // namespace sigk

@@ -1,0 +1,85 @@
+"""GPU parity of the reverse mode (reference signature_vjp,
+/root/reference/proj/src/autodiff.cpp:218-224) against the reference itself
+(compiled from its sources into oracle/_ref) and its finite differences
+(autodiff.cpp:226-266), mirroring tests/test_autodiff.cpp:73-130 and the
+acceptance gate's gradient criterion (acceptance.cpp:211-270).
+Bars: fp64 relative 1e-10 against the reference adjoint; fp32 relative 1e-4
+(two passes of fp32 accumulation over the path)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_ref():
+    if O.ref() is None:
+        pytest.skip("oracle/_ref (the compiled reference) is not built")
+
+
+def walk(B, L, d, seed, scale=None):
+    rng = np.random.default_rng(seed)
+    X = np.zeros((B, L, d))
+    if L > 1:
+        X[:, 1:] = np.cumsum(rng.standard_normal((B, L - 1, d)) * (scale or 1 / np.sqrt(L - 1)), axis=1)
+    return X
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(1e-30, np.max(np.abs(b))))
+
+
+@pytest.mark.parametrize("B,L,d,N", [(2, 2, 3, 3), (3, 7, 2, 4), (2, 33, 3, 3), (2, 50, 5, 4), (1, 20, 1, 5),
+                                     (2, 12, 4, 2), (2, 9, 2, 1)])
+def test_vjp_f64_matches_reference(sk, B, L, d, N):
+    X = walk(B, L, d, seed=B * 100 + L)
+    cot = np.random.default_rng(L).standard_normal((B, sk.sig_dim(d, N)))
+    got = sk.signature_vjp(X, N, cot)
+    ref = O.ref_vjp(X, N, cot)
+    assert got.shape == X.shape
+    assert rel(got, ref) <= 1e-10, rel(got, ref)
+
+
+def test_vjp_matches_finite_differences(sk):
+    X = walk(2, 6, 3, seed=4)
+    cot = np.random.default_rng(5).standard_normal((2, sk.sig_dim(3, 3)))
+    got = sk.signature_vjp(X, 3, cot)
+    fd = O.ref_finite_diff(X, 3, cot, 1e-5)
+    assert np.max(np.abs(got - fd)) <= 1e-6 * (1 + np.max(np.abs(fd)))
+
+
+def test_vjp_single_point_and_linearity(sk):
+    X = walk(2, 1, 3, seed=1)
+    assert not sk.signature_vjp(X, 3, np.ones((2, 39))).any()
+    X = walk(3, 40, 3, seed=2)
+    c1 = np.random.default_rng(3).standard_normal((3, 39))
+    c2 = np.random.default_rng(4).standard_normal((3, 39))
+    g = sk.signature_vjp(X, 3, 2.0 * c1 - c2)
+    assert rel(g, 2.0 * sk.signature_vjp(X, 3, c1) - sk.signature_vjp(X, 3, c2)) <= 1e-11
+
+
+def test_vjp_f32_headline_shape(sk):
+    X = walk(8, 1000, 5, seed=7)
+    cot = np.random.default_rng(8).standard_normal((8, 780))
+    ref = O.ref_vjp(X.astype(np.float32).astype(np.float64), 4, cot.astype(np.float32).astype(np.float64))
+    got = sk.signature_vjp(X.astype(np.float32), 4, cot.astype(np.float32))
+    assert rel(got, ref) <= 1e-4, rel(got, ref)
+
+
+def test_vjp_device_tensors(sk):
+    torch = pytest.importorskip("torch")
+    X = torch.from_numpy(walk(4, 64, 3, seed=9)).cuda()
+    cot = torch.randn(4, 39, dtype=torch.float64, device="cuda")
+    g = sk.signature_vjp(X, 3, cot)
+    torch.cuda.synchronize()
+    ref = O.ref_vjp(X.cpu().numpy(), 3, cot.cpu().numpy())
+    assert rel(g.cpu().numpy(), ref) <= 1e-10
+
+
+def test_vjp_shape_errors(sk):
+    with pytest.raises(sk.DomainError):
+        sk.signature_vjp(np.zeros((2, 5, 3)), 3, np.zeros((2, 38)))
+    with pytest.raises(sk.DomainError):
+        sk.signature_vjp(np.zeros((2, 5, 3)), 0, np.zeros((2, 39)))
