@@ -152,6 +152,13 @@ int sigk_brownian_f64(double* X_dev, size_t B, size_t L, int d, uint64_t seed, s
  * random walks from (seed, B, L, d), bit-identical to make_bench_paths. */
 int sigk_make_bench_paths(uint64_t seed, size_t B, size_t L, int d, double* out);
 
+/* The reference's training harness (model.cpp:222-263; paper §3.2) with the
+ * signature forward and VJP on the GPU: writes `epochs` mean losses. kernel:
+ * 0 sequential, 1 parallel, 2 auto; activation: 0 tanh, 1 identity. Returns
+ * SIGK_EDOMAIN on bad config, SIGK_EDEVICE on any other failure. */
+int sigk_train(size_t n_samples, size_t seq_len, int sig_input_size, int depth, size_t batch_size, int epochs,
+               double learning_rate, uint64_t seed, int kernel, int activation, double* epoch_losses);
+
 /* 1 when a register-sliced fast variant exists for (d, N) in this precision
  * (0: the shape-generic kernel is used). *Q receives the prefix length. */
 int sigk_has_fast_variant(int d, int N, int is_f64, int* Q);

@@ -24,3 +24,17 @@ struct DeviceError : std::runtime_error {
 };
 
 }  // namespace sigkit
+
+namespace sigkit {
+
+/// Non-finite loss during training (reference errors.hpp:22-30).
+class TrainingError : public std::runtime_error {
+public:
+    TrainingError(const std::string& what, int epoch) : std::runtime_error(what), epoch_(epoch) {}
+    int epoch() const { return epoch_; }
+
+private:
+    int epoch_;
+};
+
+}  // namespace sigkit

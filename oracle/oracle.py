@@ -94,6 +94,8 @@ def ref():
             lib.ref_random_paths.argtypes = [C.c_uint64, _sz, _sz, C.c_int, C.c_double, _dp]
             lib.ref_signature_vjp.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp, C.c_int, _dp]
             lib.ref_finite_diff_grad.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp, C.c_double, _dp]
+            lib.ref_train.argtypes = [_sz, _sz, C.c_int, C.c_int, _sz, C.c_int, C.c_double, C.c_uint64, C.c_int,
+                                      C.c_int, _dp]
             _ref = lib
     return _ref
 
@@ -239,6 +241,15 @@ def ref_vjp(X: np.ndarray, N: int, cot: np.ndarray, kernel: str = "sequential") 
     _ref_call(ref().ref_signature_vjp(_ptr(X, _dp), B, L, d, N, _ptr(cot, _dp), 1 if kernel == "parallel" else 0,
                                       _ptr(g, _dp)))
     return g
+
+
+def ref_train(n_samples, seq_len, sig_input_size, depth, batch_size, epochs, lr, seed, kernel=0,
+              activation=0) -> list[float]:
+    """The reference's training loop (model.cpp:222-263); per-epoch mean losses."""
+    out = np.empty(max(1, epochs), np.float64)
+    _ref_call(ref().ref_train(n_samples, seq_len, sig_input_size, depth, batch_size, epochs, lr, seed, kernel,
+                              activation, _ptr(out, _dp)))
+    return list(out[:epochs])
 
 
 def ref_finite_diff(X: np.ndarray, N: int, cot: np.ndarray, h: float = 1e-5) -> np.ndarray:

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "sigkit/autodiff.hpp"
+#include "sigkit/model.hpp"
 #include "helpers.hpp"  // testutil::random_paths (reference tests/helpers.hpp:16-36)
 #include "sigkit/bench.hpp"
 #include "sigkit/detail/sig_core.hpp"
@@ -207,6 +208,28 @@ int ref_finite_diff_grad(const double* x, std::size_t B, std::size_t L, int d, i
         c.values.assign(cot, cot + B * sigkit::sig_dim(d, N));
         auto g = sigkit::finite_diff_grad(make_batch(x, B, L, d), N, c, h);
         std::memcpy(grad, g.values.data(), g.values.size() * sizeof(double));
+    });
+}
+
+// train (model.cpp:222-263): the reference's training loop; writes the
+// per-epoch mean losses. kernel 0 sequential, 1 parallel, 2 auto; activation 0 tanh, 1 identity.
+int ref_train(std::size_t n_samples, std::size_t seq_len, int sig_input_size, int depth, std::size_t batch_size,
+              int epochs, double lr, std::uint64_t seed, int kernel, int activation, double* losses) {
+    return guarded([&] {
+        sigkit::TrainConfig c;
+        c.n_samples = n_samples;
+        c.seq_len = seq_len;
+        c.sig_input_size = sig_input_size;
+        c.depth = depth;
+        c.batch_size = batch_size;
+        c.epochs = epochs;
+        c.learning_rate = lr;
+        c.seed = seed;
+        c.kernel = kernel == 0 ? sigkit::KernelKind::Sequential
+                               : kernel == 1 ? sigkit::KernelKind::Parallel : sigkit::KernelKind::Auto;
+        c.activation = activation == 1 ? sigkit::Activation::Identity : sigkit::Activation::Tanh;
+        auto rep = sigkit::train(c);
+        for (std::size_t i = 0; i < rep.epoch_losses.size(); ++i) losses[i] = rep.epoch_losses[i];
     });
 }
 

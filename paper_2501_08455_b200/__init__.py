@@ -136,6 +136,8 @@ def lib():
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_uint64, sz, vp]
         L.sigk_has_fast_variant.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.sigk_plan.argtypes = [sz, sz, C.c_int, C.c_int, C.c_int, C.POINTER(_Tuning), C.POINTER(_Stats)]
+        L.sigk_train.argtypes = [sz, sz, C.c_int, C.c_int, sz, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int,
+                                 C.POINTER(C.c_double)]
         L.sigk_last_error.restype = C.c_char_p
         L.sigk_bench_ffma.argtypes = [vp, C.c_int, C.c_int, C.POINTER(C.c_double), vp]
         _lib = L
@@ -384,11 +386,40 @@ def brownian(out, seed: int = 42, row0: int = 0):
     return out
 
 
+@dataclass
+class TrainConfig:
+    """Reference ``sigkit::TrainConfig`` (include/sigkit/model.hpp:39-50)."""
+    n_samples: int = 1024
+    seq_len: int = 100
+    sig_input_size: int = 4
+    depth: int = 3
+    batch_size: int = 128
+    epochs: int = 10
+    learning_rate: float = 0.05
+    seed: int = 42
+    kernel: KernelKind = KernelKind.Auto
+    activation: str = "tanh"
+
+
+def train(config: TrainConfig) -> list[float]:
+    """Reference ``sigkit::train`` (model.cpp:222-263; paper §3.2): Dense(20->d) -> act -> signature ->
+    Dense(D->10) trained by SGD on MSE against a frozen teacher; signature forward and VJP run on the GPU.
+    Returns the per-epoch mean losses."""
+    if config.activation not in ("tanh", "identity"):
+        raise DomainError(f"unknown activation '{config.activation}', expected tanh or identity")
+    kern = {KernelKind.Sequential: 0, KernelKind.Parallel: 1}.get(config.kernel, 2)
+    losses = (C.c_double * max(1, config.epochs))()
+    _check(lib().sigk_train(config.n_samples, config.seq_len, config.sig_input_size, config.depth,
+                            config.batch_size, config.epochs, config.learning_rate, config.seed, kern,
+                            0 if config.activation == "tanh" else 1, losses))
+    return list(losses[:config.epochs])
+
+
 __all__ = [
     "DomainError", "ResourceError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
-    "signature_stream", "signature_vjp",
+    "signature_stream", "signature_vjp", "TrainConfig", "train",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
     "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES",
 ]

@@ -36,6 +36,7 @@ def _units():
                           [f"-DSIGK_REAL={real}", f"-DSIGK_DIM={d}"]))
     units.append(("sigkit_api", os.path.join(CSRC, "sigkit_api.cpp"), []))
     units.append(("bench_api", os.path.join(CSRC, "bench_api.cpp"), []))
+    units.append(("model_api", os.path.join(CSRC, "model_api.cpp"), []))
     return units
 
 

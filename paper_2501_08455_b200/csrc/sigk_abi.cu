@@ -1020,6 +1020,9 @@ int sigk_has_fast_variant(int d, int N, int is_f64, int* Q) {
 
 const char* sigk_last_error(void) { return sigk::g_err.c_str(); }
 
+// internal: lets the C++ API units report through sigk_last_error
+void sigk_internal_set_error(const char* msg) { sigk::g_err = msg; }
+
 int sigk_version(void) { return 101; }
 
 }  // extern "C"

@@ -1,29 +1,33 @@
-"""The C++ drop-in API: builds tests/cpp/test_dropin.cpp (reference test cases
-restated against include/sigkit/*.hpp) against libsigk.so; runs it on a GPU."""
+"""The C++ drop-in API: builds tests/cpp/*.cpp (reference test cases restated
+against include/sigkit/*.hpp) against libsigk.so; runs them on a GPU."""
 import os
 import subprocess
 
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
-BIN = os.path.join(ROOT, "tests", "cpp", "test_dropin")
 LIBDIR = os.path.join(ROOT, "paper_2501_08455_b200")
+CASES = ["test_dropin", "test_model_dropin"]
 
 
-def build():
-    cmd = ["g++", "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"), SRC, "-o", BIN,
+def build(name):
+    src = os.path.join(ROOT, "tests", "cpp", name + ".cpp")
+    exe = os.path.join(ROOT, "tests", "cpp", name)
+    cmd = ["g++", "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", exe,
            "-L" + LIBDIR, "-lsigk", "-Wl,-rpath," + LIBDIR]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
-    return BIN
+    return exe
 
 
-def test_dropin_headers_compile_and_link():
-    assert os.path.exists(build())
+@pytest.mark.parametrize("name", CASES)
+def test_dropin_headers_compile_and_link(name):
+    assert os.path.exists(build(name))
 
 
 @pytest.mark.gpu
-def test_dropin_reference_cases_on_gpu():
-    r = subprocess.run([build()], capture_output=True, text=True, timeout=300)
+@pytest.mark.parametrize("name", CASES)
+def test_dropin_reference_cases_on_gpu(name):
+    r = subprocess.run([build(name)], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
