@@ -55,6 +55,7 @@ extern "C" {
 #define SIGK_EDOMAIN 1
 #define SIGK_ERESOURCE 2
 #define SIGK_EDEVICE 3
+#define SIGK_ETRAINING 4 /* sigk_train only: non-finite loss (the reference's TrainingError) */
 
 /* flags for sigk_signature_*: where the buffers live. Without a flag the
  * buffer is host memory and the call is synchronous (H2D, kernels, D2H). With
@@ -155,7 +156,8 @@ int sigk_make_bench_paths(uint64_t seed, size_t B, size_t L, int d, double* out)
 /* The reference's training harness (model.cpp:222-263; paper §3.2) with the
  * signature forward and VJP on the GPU: writes `epochs` mean losses. kernel:
  * 0 sequential, 1 parallel, 2 auto; activation: 0 tanh, 1 identity. Returns
- * SIGK_EDOMAIN on bad config, SIGK_EDEVICE on any other failure. */
+ * SIGK_EDOMAIN on bad config, SIGK_ETRAINING when the loss goes non-finite,
+ * SIGK_EDEVICE on any other failure. */
 int sigk_train(size_t n_samples, size_t seq_len, int sig_input_size, int depth, size_t batch_size, int epochs,
                double learning_rate, uint64_t seed, int kernel, int activation, double* epoch_losses);
 

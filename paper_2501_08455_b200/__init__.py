@@ -26,7 +26,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SIGK_LIB_PATH: an alternative build of the same library (tuning experiments)
 LIB_PATH = os.environ.get("SIGK_LIB_PATH") or os.path.join(_HERE, "libsigk.so")
 
-SIGK_OK, SIGK_EDOMAIN, SIGK_ERESOURCE, SIGK_EDEVICE = 0, 1, 2, 3
+SIGK_OK, SIGK_EDOMAIN, SIGK_ERESOURCE, SIGK_EDEVICE, SIGK_ETRAINING = 0, 1, 2, 3, 4
 SIGK_X_ON_DEVICE, SIGK_OUT_ON_DEVICE = 1, 2
 
 
@@ -36,6 +36,15 @@ class DomainError(ValueError):
 
 class ResourceError(RuntimeError):
     """Capacity failure (reference errors.hpp:16-19)."""
+
+
+class TrainingError(RuntimeError):
+    """Reference ``sigkit::TrainingError`` (errors.hpp): non-finite loss; ``epoch`` is 0-based."""
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        tail = msg.rsplit(" ", 1)[-1]
+        self.epoch = int(tail) if tail.isdigit() else -1
 
 
 class DeviceError(RuntimeError):
@@ -152,6 +161,8 @@ def _check(rc: int):
         raise DomainError(msg)
     if rc == SIGK_ERESOURCE:
         raise ResourceError(msg)
+    if rc == SIGK_ETRAINING:
+        raise TrainingError(msg)
     raise DeviceError(msg)
 
 
@@ -416,7 +427,7 @@ def train(config: TrainConfig) -> list[float]:
 
 
 __all__ = [
-    "DomainError", "ResourceError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
+    "DomainError", "ResourceError", "TrainingError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
     "signature_stream", "signature_vjp", "TrainConfig", "train",

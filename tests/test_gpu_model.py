@@ -43,5 +43,6 @@ def test_config_validation(sk):
 
 
 def test_divergence_raises(sk):
-    with pytest.raises(sk.DeviceError, match="non-finite loss at epoch"):
+    with pytest.raises(sk.TrainingError, match="non-finite loss at epoch") as e:
         sk.train(sk.TrainConfig(**{**DESK, "epochs": 20, "learning_rate": 1e9}, activation="identity"))
+    assert 0 <= e.value.epoch < 20
