@@ -17,12 +17,14 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libsigk.so")
+# experiment builds: SIGK_DEFS="-DX=1 ..." and SIGK_LIB_OUT=path build a separate library
+DEFS = os.environ.get("SIGK_DEFS", "").split()
+OBJ = os.path.join(PKG, "_build" + ("_" + hashlib.sha1(" ".join(DEFS).encode()).hexdigest()[:8] if DEFS else ""))
+LIB = os.environ.get("SIGK_LIB_OUT") or os.path.join(PKG, "libsigk.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
-           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
+           "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + DEFS
 DIMS = [1, 2, 3, 4, 5, 6, 7, 8, 10]
 HEADERS = ["sigk_common.cuh", "fold.cuh", "merge.cuh", "pair_kernel.cuh", "ipair_kernel.cuh", "stream_kernel.cuh", "vjp_kernel.cuh", "generic.cuh", "variants.cuh", "variants.h"]
 
@@ -89,7 +91,8 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-    _build_cli(verbose)
+    if not DEFS:
+        _build_cli(verbose)
     return LIB
 
 

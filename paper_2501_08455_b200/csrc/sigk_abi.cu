@@ -608,9 +608,12 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
     }
     Real* xbuf = xdev ? const_cast<Real*>(X) : reinterpret_cast<Real*>(static_cast<char*>(stg.p) + xoff);
     Real* obuf = odev ? out : reinterpret_cast<Real*>(static_cast<char*>(stg.p) + ooff);
-    // pieces pay off once PCIe time dwarfs the per-piece API cost (~8 MB each)
+    // pieces pay off once PCIe time dwarfs the per-piece API cost: one per
+    // ~4 MB moved, >= 16 rows each, <= 8 (measured on B200, tools/e2e_ab.py:
+    // C2 2.9 MB best whole, C4 30 MB best in 4, C5 415 MB best in 8)
     const size_t moved = (xdev ? 0 : xbytes) + (odev ? 0 : obytes);
-    const int np = (int)std::max<size_t>(1, std::min<size_t>({(size_t)Staging::kPieces, B / 32, moved >> 23}));
+    int np = (int)std::max<size_t>(1, std::min<size_t>({(size_t)Staging::kPieces, B / 16, moved >> 22}));
+    if (const char* f = getenv("SIGK_HOST_PIECES")) np = std::max(1, std::min(Staging::kPieces, atoi(f)));  // experiments
     const size_t per = (B + np - 1) / np;
     // the copy streams start after everything already queued on the caller's stream
     cudaEventRecord(stg.ev[2 * Staging::kPieces], s);
