@@ -153,6 +153,17 @@ int sigk_brownian_f64(double* X_dev, size_t B, size_t L, int d, uint64_t seed, s
  * random walks from (seed, B, L, d), bit-identical to make_bench_paths. */
 int sigk_make_bench_paths(uint64_t seed, size_t B, size_t L, int d, double* out);
 
+/* Increments X[:, k+1] - X[:, k] into out (B, L-1, d) (reference
+ * increments, kernels.cpp:71-87), and increments divided by m! for m =
+ * 2..depth into out (depth-1, n) (reference scaled_increments,
+ * kernels.cpp:89-104). Elementwise GPU kernels, fp64 bit-identical to the
+ * reference. Flags and stream as for sigk_signature_*; host buffers make the
+ * call synchronous. L = 1 / depth = 1 write nothing. */
+int sigk_increments_f32(const float* X, size_t B, size_t L, int d, float* out, unsigned flags, void* stream);
+int sigk_increments_f64(const double* X, size_t B, size_t L, int d, double* out, unsigned flags, void* stream);
+int sigk_scaled_increments_f32(const float* inc, size_t n, int depth, float* out, unsigned flags, void* stream);
+int sigk_scaled_increments_f64(const double* inc, size_t n, int depth, double* out, unsigned flags, void* stream);
+
 /* The reference's training harness (model.cpp:222-263; paper §3.2) with the
  * signature forward and VJP on the GPU: writes `epochs` mean losses. kernel:
  * 0 sequential, 1 parallel, 2 auto; activation: 0 tanh, 1 identity. Returns

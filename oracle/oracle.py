@@ -94,6 +94,8 @@ def ref():
             lib.ref_random_paths.argtypes = [C.c_uint64, _sz, _sz, C.c_int, C.c_double, _dp]
             lib.ref_signature_vjp.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp, C.c_int, _dp]
             lib.ref_finite_diff_grad.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp, C.c_double, _dp]
+            lib.ref_increments.argtypes = [_dp, _sz, _sz, C.c_int, _dp]
+            lib.ref_scaled_increments.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp]
             lib.ref_train.argtypes = [_sz, _sz, C.c_int, C.c_int, _sz, C.c_int, C.c_double, C.c_uint64, C.c_int,
                                       C.c_int, _dp]
             _ref = lib
@@ -241,6 +243,24 @@ def ref_vjp(X: np.ndarray, N: int, cot: np.ndarray, kernel: str = "sequential") 
     _ref_call(ref().ref_signature_vjp(_ptr(X, _dp), B, L, d, N, _ptr(cot, _dp), 1 if kernel == "parallel" else 0,
                                       _ptr(g, _dp)))
     return g
+
+
+def ref_increments(X: np.ndarray) -> np.ndarray:
+    """The reference's increments (kernels.cpp:71-87)."""
+    X = np.ascontiguousarray(X, np.float64)
+    B, L, d = X.shape
+    out = np.empty((B, L - 1, d))
+    _ref_call(ref().ref_increments(_ptr(X, _dp), B, L, d, _ptr(out, _dp)))
+    return out
+
+
+def ref_scaled_increments(inc: np.ndarray, depth: int) -> list:
+    """The reference's scaled_increments (kernels.cpp:89-104)."""
+    inc = np.ascontiguousarray(inc, np.float64)
+    B, S, d = inc.shape
+    out = np.empty((max(0, depth - 1), B, S, d))
+    _ref_call(ref().ref_scaled_increments(_ptr(inc, _dp), B, S, d, depth, _ptr(out, _dp)))
+    return list(out)
 
 
 def ref_train(n_samples, seq_len, sig_input_size, depth, batch_size, epochs, lr, seed, kernel=0,

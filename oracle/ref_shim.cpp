@@ -211,6 +211,26 @@ int ref_finite_diff_grad(const double* x, std::size_t B, std::size_t L, int d, i
     });
 }
 
+// increments / scaled_increments (kernels.cpp:71-104)
+int ref_increments(const double* x, std::size_t B, std::size_t L, int d, double* out) {
+    return guarded([&] {
+        auto inc = sigkit::increments(make_batch(x, B, L, d));
+        std::memcpy(out, inc.diffs.data(), inc.diffs.size() * sizeof(double));
+    });
+}
+int ref_scaled_increments(const double* diffs, std::size_t B, std::size_t S, int d, int depth, double* out) {
+    return guarded([&] {
+        sigkit::IncrementBatch inc;
+        inc.batch = B;
+        inc.segments = S;
+        inc.dim = d;
+        inc.diffs.assign(diffs, diffs + B * S * static_cast<std::size_t>(d));
+        auto sc = sigkit::scaled_increments(inc, depth);
+        for (std::size_t m = 0; m < sc.per_degree.size(); ++m)
+            std::memcpy(out + m * inc.diffs.size(), sc.per_degree[m].data(), inc.diffs.size() * sizeof(double));
+    });
+}
+
 // train (model.cpp:222-263): the reference's training loop; writes the
 // per-epoch mean losses. kernel 0 sequential, 1 parallel, 2 auto; activation 0 tanh, 1 identity.
 int ref_train(std::size_t n_samples, std::size_t seq_len, int sig_input_size, int depth, std::size_t batch_size,

@@ -145,6 +145,10 @@ def lib():
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_uint64, sz, vp]
         L.sigk_has_fast_variant.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
         L.sigk_plan.argtypes = [sz, sz, C.c_int, C.c_int, C.c_int, C.POINTER(_Tuning), C.POINTER(_Stats)]
+        for n in ("sigk_increments_f32", "sigk_increments_f64"):
+            getattr(L, n).argtypes = [vp, sz, sz, C.c_int, vp, C.c_uint, vp]
+        for n in ("sigk_scaled_increments_f32", "sigk_scaled_increments_f64"):
+            getattr(L, n).argtypes = [vp, sz, C.c_int, vp, C.c_uint, vp]
         L.sigk_train.argtypes = [sz, sz, C.c_int, C.c_int, sz, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int,
                                  C.POINTER(C.c_double)]
         L.sigk_last_error.restype = C.c_char_p
@@ -397,6 +401,38 @@ def brownian(out, seed: int = 42, row0: int = 0):
     return out
 
 
+def increments(paths):
+    """Reference ``increments`` (kernels.cpp:71-87): X[:, k+1] - X[:, k], (B, L-1, d), on the GPU.
+    numpy in -> numpy out; CUDA tensors in -> CUDA tensor out."""
+    if _is_torch(paths):
+        import torch
+
+        B, L, d = _validate_shape(paths.shape, 1)
+        X = paths.contiguous()
+        out = torch.empty((B, L - 1, d), dtype=X.dtype, device=X.device)
+        fn = lib().sigk_increments_f32 if X.dtype == torch.float32 else lib().sigk_increments_f64
+        with torch.cuda.device(X.device):
+            _check(fn(X.data_ptr(), B, L, d, out.data_ptr(), SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE,
+                      torch.cuda.current_stream(X.device).cuda_stream))
+        return out
+    X = np.asarray(paths)
+    B, L, d = _validate_shape(X.shape, 1)
+    X = np.ascontiguousarray(X if X.dtype in (np.float32, np.float64) else X.astype(np.float64))
+    out = np.empty((B, L - 1, d), X.dtype)
+    fn = lib().sigk_increments_f32 if X.dtype == np.float32 else lib().sigk_increments_f64
+    _check(fn(X.ctypes.data, B, L, d, out.ctypes.data if out.size else None, 0, None))
+    return out
+
+
+def scaled_increments(inc, depth: int) -> list:
+    """Reference ``scaled_increments`` (kernels.cpp:89-104): [inc / m! for m = 2..depth] on the GPU."""
+    a = np.ascontiguousarray(inc if np.asarray(inc).dtype in (np.float32, np.float64) else np.asarray(inc, np.float64))
+    out = np.empty((max(0, depth - 1),) + a.shape, a.dtype)
+    fn = lib().sigk_scaled_increments_f32 if a.dtype == np.float32 else lib().sigk_scaled_increments_f64
+    _check(fn(a.ctypes.data if a.size else None, a.size, depth, out.ctypes.data if out.size else None, 0, None))
+    return list(out)
+
+
 @dataclass
 class TrainConfig:
     """Reference ``sigkit::TrainConfig`` (include/sigkit/model.hpp:39-50)."""
@@ -430,7 +466,7 @@ __all__ = [
     "DomainError", "ResourceError", "TrainingError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
-    "signature_stream", "signature_vjp", "TrainConfig", "train",
+    "signature_stream", "signature_vjp", "TrainConfig", "train", "increments", "scaled_increments",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
     "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES",
 ]

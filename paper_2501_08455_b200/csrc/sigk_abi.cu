@@ -18,6 +18,7 @@
 #include "generic.cuh"
 #include "variants.h"
 #include "vjp_kernel.cuh"
+#include "increments.cuh"
 
 namespace sigk {
 
@@ -653,6 +654,63 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
     return rc;
 }
 
+// Elementwise utilities (increments, scaled increments): device buffers run
+// asynchronously on `stream`; host buffers go through a stream-ordered
+// device copy and the call returns when the result is back.
+template <typename Real, typename Launch>
+static int elementwise_call(const Real* in, size_t n_in, Real* out, size_t n_out, unsigned flags, void* stream,
+                            Launch&& launch) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool idev = flags & SIGK_X_ON_DEVICE, odev = flags & SIGK_OUT_ON_DEVICE;
+    Real *din = const_cast<Real*>(in), *dout = out;
+    cudaError_t e = cudaSuccess;
+    if (!idev && n_in) {
+        e = cudaMallocAsync(reinterpret_cast<void**>(&din), n_in * sizeof(Real), s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(din, in, n_in * sizeof(Real), cudaMemcpyHostToDevice, s);
+    }
+    if (e == cudaSuccess && !odev && n_out) e = cudaMallocAsync(reinterpret_cast<void**>(&dout), n_out * sizeof(Real), s);
+    if (e == cudaSuccess && n_out) {
+        launch(din, dout, s);
+        e = cudaPeekAtLastError();
+    }
+    if (e == cudaSuccess && !odev && n_out) e = cudaMemcpyAsync(out, dout, n_out * sizeof(Real), cudaMemcpyDeviceToHost, s);
+    if (!idev && n_in && din) cudaFreeAsync(din, s);
+    if (!odev && n_out && dout) cudaFreeAsync(dout, s);
+    if (e == cudaSuccess && !(idev && odev)) e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? SIGK_OK : cuda_fail(e, "elementwise kernel");
+}
+
+static unsigned elementwise_grid(size_t n) {
+    const size_t want = (n + 255) / 256;
+    return (unsigned)std::max<size_t>(1, std::min<size_t>(want, 148 * 16));
+}
+
+template <typename Real>
+static int increments_impl(const Real* X, size_t B, size_t L, int d, Real* out, unsigned flags, void* stream) {
+    g_err.clear();
+    if (B < 1 || L < 1 || d < 1) return fail(SIGK_EDOMAIN, "paths: batch, len and dim must all be >= 1");
+    if (X == nullptr || (out == nullptr && L > 1)) return fail(SIGK_EDOMAIN, "paths/out pointer is null");
+    const size_t n_out = B * (L - 1) * (size_t)d;
+    return elementwise_call<Real>(X, n_out ? B * L * (size_t)d : 0, out, n_out, flags, stream,
+                                  [&](const Real* din, Real* dout, cudaStream_t s) {
+                                      increments_kernel<Real><<<elementwise_grid(n_out), 256, 0, s>>>(
+                                          din, (int64_t)B, (int64_t)L, d, dout);
+                                  });
+}
+
+template <typename Real>
+static int scaled_increments_impl(const Real* inc, size_t n, int depth, Real* out, unsigned flags, void* stream) {
+    g_err.clear();
+    if (depth < 1) return fail(SIGK_EDOMAIN, "depth must be >= 1, got " + std::to_string(depth));
+    const size_t n_out = n * (size_t)(depth - 1);
+    if (n_out && (inc == nullptr || out == nullptr)) return fail(SIGK_EDOMAIN, "increments/out pointer is null");
+    return elementwise_call<Real>(inc, n_out ? n : 0, out, n_out, flags, stream,
+                                  [&](const Real* din, Real* dout, cudaStream_t s) {
+                                      scaled_increments_kernel<Real><<<elementwise_grid(n), 256, 0, s>>>(
+                                          din, (int64_t)n, depth, dout);
+                                  });
+}
+
 // Prefix stream (reference signature_stream, kernels.cpp:156-198): out is
 // (B, L-1, D), row t = signature of X[0..t+1]. fp32 shapes with a pair
 // variant use the two-pass chunk-pair stream kernel (stream_kernel.cuh); the
@@ -963,6 +1021,19 @@ int sigk_signature_f32(const float* X, size_t B, size_t L, int d, int N, float* 
 int sigk_signature_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags, void* stream,
                        const sigk_tuning* tuning, sigk_stats* stats) {
     return sigk::signature_impl<double>(X, B, L, d, N, out, flags, stream, tuning, stats);
+}
+
+int sigk_increments_f32(const float* X, size_t B, size_t L, int d, float* out, unsigned flags, void* stream) {
+    return sigk::increments_impl<float>(X, B, L, d, out, flags, stream);
+}
+int sigk_increments_f64(const double* X, size_t B, size_t L, int d, double* out, unsigned flags, void* stream) {
+    return sigk::increments_impl<double>(X, B, L, d, out, flags, stream);
+}
+int sigk_scaled_increments_f32(const float* inc, size_t n, int depth, float* out, unsigned flags, void* stream) {
+    return sigk::scaled_increments_impl<float>(inc, n, depth, out, flags, stream);
+}
+int sigk_scaled_increments_f64(const double* inc, size_t n, int depth, double* out, unsigned flags, void* stream) {
+    return sigk::scaled_increments_impl<double>(inc, n, depth, out, flags, stream);
 }
 
 int sigk_signature_stream_f32(const float* X, size_t B, size_t L, int d, int N, float* out, unsigned flags,

@@ -186,6 +186,36 @@ KernelKind select_kernel(KernelKind hint, const ExecutionCaps& caps, std::size_t
     return (caps.accelerated && seq_len >= caps.parallel_min_len) ? KernelKind::Parallel : KernelKind::Sequential;
 }
 
+IncrementBatch increments(const PathBatch& paths) {
+    validate_paths(paths);
+    IncrementBatch inc;
+    inc.batch = paths.batch;
+    inc.segments = paths.len - 1;
+    inc.dim = paths.dim;
+    inc.diffs.resize(inc.batch * inc.segments * static_cast<std::size_t>(inc.dim));
+    const int rc = sigk_increments_f64(paths.values.data(), paths.batch, paths.len, paths.dim, inc.diffs.data(), 0u,
+                                       nullptr);
+    if (rc != SIGK_OK) rethrow(rc);
+    return inc;
+}
+
+ScaledIncrements scaled_increments(const IncrementBatch& inc, int depth) {
+    validate_depth(depth);
+    ScaledIncrements sc;
+    sc.batch = inc.batch;
+    sc.segments = inc.segments;
+    sc.dim = inc.dim;
+    sc.depth = depth;
+    const std::size_t n = inc.diffs.size();
+    std::vector<double> all(n * static_cast<std::size_t>(depth - 1));
+    const int rc = sigk_scaled_increments_f64(inc.diffs.data(), n, depth, all.data(), 0u, nullptr);
+    if (rc != SIGK_OK) rethrow(rc);
+    for (int m = 2; m <= depth; ++m)
+        sc.per_degree.emplace_back(all.begin() + static_cast<std::ptrdiff_t>((m - 2) * n),
+                                   all.begin() + static_cast<std::ptrdiff_t>((m - 1) * n));
+    return sc;
+}
+
 SignatureBatch signature_sequential(const PathBatch& paths, int depth, KernelStats* stats) {
     return run_gpu(paths, depth, stats);
 }

@@ -142,6 +142,25 @@ int main() {
         CHECK(threw);
     }
 
+    // increments / scaled_increments (kernels.cpp:71-104; test_kernels.cpp increment cases)
+    {
+        const PathBatch p = random_paths(77, 3, 9, 2, 0.5);
+        const IncrementBatch inc = increments(p);
+        CHECK(inc.batch == 3 && inc.segments == 8 && inc.dim == 2 && inc.diffs.size() == 48);
+        bool exact = true;
+        for (std::size_t b = 0; b < 3; ++b)
+            for (std::size_t k = 0; k < 8; ++k)
+                for (int c = 0; c < 2; ++c)
+                    exact &= inc.diffs[(b * 8 + k) * 2 + c] == p.at(b, k + 1, c) - p.at(b, k, c);
+        CHECK(exact);
+        const ScaledIncrements sc = scaled_increments(inc, 4);
+        CHECK(sc.per_degree.size() == 3 && sc.depth == 4);
+        CHECK(sc.per_degree[2][5] == inc.diffs[5] / 24.0);
+        PathBatch one = random_paths(78, 2, 1, 3, 1.0);
+        CHECK(increments(one).diffs.empty());
+        CHECK(scaled_increments(increments(p), 1).per_degree.empty());
+    }
+
     std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
     return failures ? 1 : 0;
 }
