@@ -5,15 +5,39 @@
 // fp64 results are bit-identical.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 namespace sigk {
 
-// out (B, L-1, d): out[b, k, c] = X[b, k+1, c] - X[b, k, c]
+// out (B, L-1, d): out[b, k, c] = X[b, k+1, c] - X[b, k, c]. Path b's
+// output is its input shifted by d elements, so each path is a contiguous
+// run: vector loads of 16 bytes (float4 / double2) when the run and both
+// pointers are 16-byte aligned, scalar otherwise (the two loads of an
+// element hit the same or neighbouring sectors; L2 absorbs the overlap).
 template <typename Real>
 __global__ void increments_kernel(const Real* __restrict__ X, int64_t B, int64_t L, int d, Real* __restrict__ out) {
     const int64_t row = (L - 1) * d;  // output elements per path
     const int64_t n = B * row;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    constexpr int V = 16 / sizeof(Real);
+    using Vec = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
+    const bool vec = (row % V == 0) && (d % V == 0) && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(out)) % 16 == 0);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (vec) {
+        const int64_t nv = n / V, rowv = row / V, dv = d / V;
+        const Vec* Xv = reinterpret_cast<const Vec*>(X);
+        Vec* ov = reinterpret_cast<Vec*>(out);
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+            const int64_t b = i / rowv, r = i - b * rowv;
+            const Vec* src = Xv + b * (rowv + dv) + r;  // path b starts at b*L*d = b*(row + d)
+            const Vec lo = src[0], hi = src[dv];
+            Vec o;
+            if constexpr (sizeof(Real) == 4) o = make_float4(hi.x - lo.x, hi.y - lo.y, hi.z - lo.z, hi.w - lo.w);
+            else o = make_double2(hi.x - lo.x, hi.y - lo.y);
+            ov[i] = o;
+        }
+        return;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
         const int64_t b = i / row, r = i - b * row;
         const Real* src = X + b * L * d + r;
         out[i] = src[d] - src[0];

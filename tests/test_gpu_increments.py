@@ -18,7 +18,7 @@ def need_ref():
         pytest.skip("oracle/_ref (the compiled reference) is not built")
 
 
-@pytest.mark.parametrize("B,L,d", [(1, 2, 1), (3, 7, 2), (5, 100, 5), (2, 1, 3), (65, 33, 10)])
+@pytest.mark.parametrize("B,L,d", [(1, 2, 1), (3, 7, 2), (5, 100, 5), (2, 1, 3), (65, 33, 10), (7, 50, 4), (3, 9, 8)])
 def test_increments_match_reference(sk, B, L, d):
     X = np.random.default_rng(B * L + d).standard_normal((B, L, d))
     got = sk.increments(X)
