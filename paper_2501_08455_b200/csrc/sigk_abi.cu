@@ -844,37 +844,100 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             return rc;
         }
     }
+    // chunk the steps so B*U CTAs fill the GPU: chunk signatures (the forward
+    // kernels on the gathered chunks) give the cotangent at every chunk end
+    const int sms = device_info([] { int v = 0; cudaGetDevice(&v); return v; }()).sms;
+    int U = 1;
+    if (M >= 32 && (tun == nullptr || tun->chunks != 1)) {
+        const int64_t want = ((int64_t)sms * 8 + B - 1) / B;
+        U = (int)std::max<int64_t>(1, std::min<int64_t>(want, M / 16));
+        if (tun && tun->chunks > 1) U = (int)std::min<int64_t>(tun->chunks, M);
+    }
+    const int64_t CL = M > 0 ? (M + U - 1) / U : 1;
+    if (M > 0) U = (int)((M + CL - 1) / CL);
+    std::vector<void*> tmp;
+    auto alloc = [&](void** ptr, size_t bytes) {
+        cudaError_t ea = cudaMallocAsync(ptr, std::max<size_t>(bytes, 16), s);
+        if (ea == cudaSuccess) tmp.push_back(*ptr);
+        return ea;
+    };
+    auto release = [&] {
+        for (void* q : tmp) cudaFreeAsync(q, s);
+        if (states) cudaFreeAsync(states, s);
+    };
+    int launches = 0;
+    const Real* cbars = cot;
+    if (U > 1) {
+        Real *Xseg = nullptr, *C = nullptr, *cb = nullptr;
+        e = alloc(reinterpret_cast<void**>(&Xseg), sizeof(Real) * B * U * (CL + 1) * d);
+        if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&C), sizeof(Real) * B * U * D);
+        if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&cb), sizeof(Real) * B * U * D);
+        if (e != cudaSuccess) {
+            release();
+            return cuda_fail(e, "vjp chunk allocation");
+        }
+        segment_gather_kernel<Real><<<sms * 8, 256, 0, s>>>(X, B, L, d, U, CL, Xseg);
+        sigk_stats cst{};
+        const int rc = run_device<Real>(Xseg, B * U, CL + 1, d, N, C, s, nullptr, &cst);
+        if (rc != SIGK_OK) {
+            release();
+            return rc;
+        }
+        vjp_boundary_kernel<Real><<<(unsigned)B, 256, 0, s>>>(C, cot, cb, U, d, N, D);
+        cbars = cb;
+        launches += 2 + cst.launches;
+    }
+    Real* dbar = nullptr;
+    if (M > 0 && (e = alloc(reinterpret_cast<void**>(&dbar), sizeof(Real) * B * M * d)) != cudaSuccess) {
+        release();
+        return cuda_fail(e, "vjp allocation");
+    }
     const size_t work = sizeof(Real) * vjp_work_elems(D, d);
     const int use_smem = work <= 160 * 1024;
     Real* gwork = nullptr;
     if (!use_smem) {
-        e = cudaMallocAsync(reinterpret_cast<void**>(&gwork), work * B, s);
+        e = alloc(reinterpret_cast<void**>(&gwork), work * B * U);
         if (e != cudaSuccess) {
-            if (states) cudaFreeAsync(states, s);
+            release();
             return cuda_fail(e, "vjp work allocation");
         }
     } else if (work > 48 * 1024) {
         cudaFuncSetAttribute(vjp_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)work);
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)B);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = use_smem ? work : 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;  // the kernel waits for its predecessor (the states) before reading anything
-    e = cudaLaunchKernelEx(&cfg, vjp_kernel<Real>, X, L, d, N, D, static_cast<const Real*>(states), cot, grad, gwork,
-                           use_smem);
-    if (states) cudaFreeAsync(states, s);
-    if (gwork) cudaFreeAsync(gwork, s);
+    if (M > 0) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(B * U));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = use_smem ? work : 0;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;  // the kernel waits for its predecessor before reading anything
+        e = cudaLaunchKernelEx(&cfg, vjp_kernel<Real>, X, L, d, N, D, static_cast<const Real*>(states), cbars, U, CL,
+                               dbar, gwork, use_smem);
+        if (e != cudaSuccess) {
+            release();
+            return cuda_fail(e, "vjp launch");
+        }
+        launches += 1;
+    }
+    const int64_t ng = B * L * d;
+    vjp_grad_kernel<Real><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((ng + 255) / 256, sms * 16)), 256, 0, s>>>(
+        dbar, B, L, d, grad);
+    launches += 1;
+    e = cudaPeekAtLastError();
+    release();
     if (e != cudaSuccess) return cuda_fail(e, "vjp launch");
     int dev = 0;
     cudaGetDevice(&dev);
     may_overlap_previous(dev, s, X, 0, grad, sizeof(Real) * B * L * d);
-    if (st) st->launches += 1;
+    if (st) {
+        st->launches += launches;
+        st->chunks = U;
+        st->fold_steps = CL;
+    }
     return SIGK_OK;
 }
 

@@ -45,17 +45,23 @@ __device__ __forceinline__ void prefetch_row(Real* dst, const Real* src, int64_t
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
+// CTA (b, j) of the grid walks chunk j = steps [j*CL, min((j+1)*CL, M)) of
+// path b backwards, starting from the cotangent of the state at the chunk's
+// end (cbars row b*U + j; the boundary kernel below), and writes δ̄_s of its
+// steps to dbar (B, M, d); vjp_grad_kernel turns those into ∂/∂X.
 template <typename Real>
 __global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, int64_t L, int d, int N, int64_t D,
-                                                  const Real* __restrict__ states, const Real* __restrict__ cot,
-                                                  Real* __restrict__ grad, Real* __restrict__ gwork, int use_smem) {
+                                                  const Real* __restrict__ states, const Real* __restrict__ cbars,
+                                                  int U, int64_t CL, Real* __restrict__ dbar,
+                                                  Real* __restrict__ gwork, int use_smem) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int64_t off[kGenericMaxDepth + 1];
     __shared__ Real invfact[kGenericMaxDepth + 1];
-    const int64_t b = blockIdx.x;
+    const int64_t b = blockIdx.x / U, j = blockIdx.x - (blockIdx.x / U) * U;
     const int64_t M = L - 1;
+    const int64_t s_lo = j * CL < M ? j * CL : M, s_hi = (j + 1) * CL < M ? (j + 1) * CL : M;
     const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
-    Real* work = use_smem ? reinterpret_cast<Real*>(smem_raw) : gwork + b * vjp_work_elems(D, d);
+    Real* work = use_smem ? reinterpret_cast<Real*>(smem_raw) : gwork + (int64_t)blockIdx.x * vjp_work_elems(D, d);
     Real* cbar = work;            // [D] cotangent of the state after the step
     Real* abar = cbar + D;        // [D] ... of the state before it
     Real* ebar = abar + D;        // [D] ... of exp(δ)
@@ -80,22 +86,19 @@ __global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, in
     pdl_wait();
     const Real* xb = X + b * L * d;
     const Real* sb = states + b * M * D;
-    Real* gb = grad + b * L * d;
-    for (int64_t i = tid; i < D; i += nth) cbar[i] = cot[b * D + i];
-    for (int c = tid; c < d; c += nth) dbn[c] = Real(0);
-    if (M == 0)
-        for (int c = tid; c < d; c += nth) gb[c] = Real(0);
+    Real* db_out = dbar + b * M * d;
+    for (int64_t i = tid; i < D; i += nth) cbar[i] = cbars[(int64_t)blockIdx.x * D + i];
     const bool async_rows = use_smem;
-    if (async_rows && M >= 2) prefetch_row(Ab[(M - 1) & 1], sb + (M - 2) * D, D);
+    if (async_rows && s_hi > s_lo && s_hi >= 2) prefetch_row(Ab[(s_hi - 1) & 1], sb + (s_hi - 2) * D, D);
     __syncthreads();
-    for (int64_t s = M - 1; s >= 0; --s) {
+    for (int64_t s = s_hi - 1; s >= s_lo; --s) {
         // state before step s (null: identity); the row for step s-1 streams in meanwhile
         const Real* A = nullptr;
         if (s > 0) {
             if (async_rows) {
                 asm volatile("cp.async.wait_all;" ::: "memory");
                 A = Ab[s & 1];
-                if (s >= 2) prefetch_row(Ab[(s - 1) & 1], sb + (s - 2) * D, D);
+                if (s >= 2 && s - 1 >= s_lo) prefetch_row(Ab[(s - 1) & 1], sb + (s - 2) * D, D);
             } else {
                 A = sb + (s - 1) * D;
             }
@@ -195,16 +198,80 @@ __global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, in
             }
             __syncthreads();
         }
-        for (int c = tid; c < d; c += nth) {
-            const Real v = db[c] + ebar[c];
-            gb[(s + 1) * d + c] = v - dbn[c];
-            if (s == 0) gb[c] = -v;
-            dbn[c] = v;
-        }
+        for (int c = tid; c < d; c += nth) db_out[s * d + c] = db[c] + ebar[c];  // δ̄_s
         Real* t = cbar;
         cbar = abar;
         abar = t;
         __syncthreads();
+    }
+}
+
+// Xseg (B*U, CL+1, d): chunk j of path b as its own path (the last point is
+// repeated past the end: zero increments, identity factors).
+template <typename Real>
+__global__ void segment_gather_kernel(const Real* __restrict__ X, int64_t B, int64_t L, int d, int U, int64_t CL,
+                                      Real* __restrict__ Xseg) {
+    const int64_t per = (CL + 1) * d, n = B * U * per;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / per, q = i - r * per, b = r / U, j = r - b * U;
+        const int64_t t = j * CL + q / d, c = q - (q / d) * d;
+        Xseg[i] = X[(b * L + (t < L - 1 ? t : L - 1)) * d + c];
+    }
+}
+
+// Cotangents of the state at every chunk end, one CTA per path: row U-1 is
+// the output cotangent, row j-1 = row j pulled back through right
+// multiplication by chunk j's signature C_j (the adjoint the per-step loop
+// applies with exp(δ)): Ā_n[I] = Ā'_n[I] + Σ_k Σ_J Ā'_{n+k}[I J] C_k[J].
+template <typename Real>
+__global__ void __launch_bounds__(256) vjp_boundary_kernel(const Real* __restrict__ C, const Real* __restrict__ cot,
+                                                           Real* __restrict__ cbars, int U, int d, int N, int64_t D) {
+    __shared__ int64_t off[kGenericMaxDepth + 1];
+    const int64_t b = blockIdx.x;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    if (tid == 0) {
+        off[0] = 0;
+        int64_t p = 1;
+        for (int n = 1; n <= N; ++n) {
+            p *= d;
+            off[n] = off[n - 1] + p;
+        }
+    }
+    pdl_trigger();
+    pdl_wait();
+    Real* cb = cbars + b * U * D;
+    for (int64_t i = tid; i < D; i += nth) cb[(int64_t)(U - 1) * D + i] = cot[b * D + i];
+    __syncthreads();
+    for (int j = U - 1; j >= 1; --j) {
+        const Real* src = cb + (int64_t)j * D;
+        const Real* cj = C + (b * U + j) * D;
+        Real* dst = cb + (int64_t)(j - 1) * D;
+        for (int n = 1; n <= N; ++n) {
+            const int64_t sz = off[n] - off[n - 1];
+            for (int64_t I = tid; I < sz; I += nth) {
+                Real acc = src[off[n - 1] + I];
+                int64_t w = 1;
+                for (int k = 1; n + k <= N; ++k) {
+                    w *= d;
+                    const Real* cr = src + off[n + k - 1] + I * w;
+                    const Real* er = cj + off[k - 1];
+                    for (int64_t J = 0; J < w; ++J) acc = fma(cr[J], er[J], acc);
+                }
+                dst[off[n - 1] + I] = acc;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ∂/∂X_t = δ̄_{t-1} - δ̄_t (δ̄_{-1} = δ̄_M = 0), grad (B, L, d)
+template <typename Real>
+__global__ void vjp_grad_kernel(const Real* __restrict__ dbar, int64_t B, int64_t L, int d, Real* __restrict__ grad) {
+    const int64_t M = L - 1, n = B * L * d;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / (L * d), q = i - b * L * d, t = q / d, c = q - t * d;
+        const Real* db = dbar + b * M * d;
+        grad[i] = (t >= 1 ? db[(t - 1) * d + c] : Real(0)) - (t < M ? db[t * d + c] : Real(0));
     }
 }
 
