@@ -344,6 +344,12 @@ static void* segment_scratch(int dev, cudaStream_t s, int kind, size_t bytes, bo
         return p;
     }
     const size_t n = std::max(bytes, hit ? 2 * hit->n : bytes);
+    if (hit) {  // growth is rare: retire the old buffer once the stream is done with it
+        cudaStreamSynchronize(s);
+        cudaFree(hit->p);
+        hit->p = nullptr;
+        hit->n = 0;
+    }
     void* p = nullptr;
     if (cudaMalloc(&p, n) != cudaSuccess) return nullptr;
     if (kind == 1 && cudaMemset(p, 0, n) != cudaSuccess) return nullptr;
@@ -834,13 +840,32 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     }
     const int64_t M = L - 1;
     cudaError_t e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    // working buffers persist per (device, stream) across calls (a stream-ordered
+    // allocation per call would be unmapped at every synchronize and re-mapped)
+    std::vector<void*> tmp;
+    int next_kind = 2;
+    auto alloc = [&](void** ptr, size_t bytes) {
+        bool async_alloc = false;
+        *ptr = segment_scratch(dev, s, next_kind++, std::max<size_t>(bytes, 16), cap != cudaStreamCaptureStatusNone,
+                               &async_alloc);
+        if (*ptr == nullptr) return cudaErrorMemoryAllocation;
+        if (async_alloc) tmp.push_back(*ptr);
+        return cudaSuccess;
+    };
+    auto release = [&] {
+        for (void* q : tmp) cudaFreeAsync(q, s);
+    };
     Real* states = nullptr;
     if (M > 0) {
-        e = cudaMallocAsync(reinterpret_cast<void**>(&states), sizeof(Real) * B * M * D, s);
+        e = alloc(reinterpret_cast<void**>(&states), sizeof(Real) * B * M * D);
         if (e != cudaSuccess) return cuda_fail(e, "vjp state allocation");
         const int rc = stream_device<Real>(X, B, L, d, N, states, s, tun, st);
         if (rc != SIGK_OK) {
-            cudaFreeAsync(states, s);
+            release();
             return rc;
         }
     }
@@ -855,16 +880,6 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     }
     const int64_t CL = M > 0 ? (M + U - 1) / U : 1;
     if (M > 0) U = (int)((M + CL - 1) / CL);
-    std::vector<void*> tmp;
-    auto alloc = [&](void** ptr, size_t bytes) {
-        cudaError_t ea = cudaMallocAsync(ptr, std::max<size_t>(bytes, 16), s);
-        if (ea == cudaSuccess) tmp.push_back(*ptr);
-        return ea;
-    };
-    auto release = [&] {
-        for (void* q : tmp) cudaFreeAsync(q, s);
-        if (states) cudaFreeAsync(states, s);
-    };
     int launches = 0;
     const Real* cbars = cot;
     if (U > 1) {
@@ -907,7 +922,10 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     if (M > 0) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(B * U));
-        cfg.blockDim = dim3(256);
+        // most per-step loops are level-sized (d^n items): small blocks keep lanes busy;
+        // SIGK_VJP_THREADS overrides (experiments)
+        const char* vt = getenv("SIGK_VJP_THREADS");
+        cfg.blockDim = dim3(vt ? (unsigned)atoi(vt) : 128u);  // measured: 128 beats 64 and 256 (C2, d=10 N=3)
         cfg.dynamicSmemBytes = use_smem ? work : 0;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
@@ -930,8 +948,6 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     e = cudaPeekAtLastError();
     release();
     if (e != cudaSuccess) return cuda_fail(e, "vjp launch");
-    int dev = 0;
-    cudaGetDevice(&dev);
     may_overlap_previous(dev, s, X, 0, grad, sizeof(Real) * B * L * d);
     if (st) {
         st->launches += launches;
