@@ -557,7 +557,7 @@ __device__ __forceinline__ void segment_combine_path(const float* __restrict__ R
 template <typename PF>
 __device__ __forceinline__ float* pair_stage_and_table(const float* __restrict__ xb, int64_t seg0, int64_t slen,
                                                        int CL, int UP, f2* __restrict__ tab, float* raw,
-                                                       uint64_t* bar) {
+                                                       uint64_t* bar, long long* staged_stamp = nullptr) {
     constexpr int d = PF::d, RS = PF::RS, RP = PF::RP, NR = PF::NR;
     const int tid = threadIdx.x, nth = blockDim.x;
     // 1. stage the segment's points X[seg0 .. seg0+slen]: one TMA bulk copy of
@@ -598,6 +598,7 @@ __device__ __forceinline__ float* pair_stage_and_table(const float* __restrict__
         }
     }
     __syncthreads();
+    if (staged_stamp != nullptr && threadIdx.x == 0) *staged_stamp = clock64();  // probes: staging done
     // 2. the operand table: row (s, kk) = (δ_{2kk}[c]/m, δ_{2kk+1}[c]/m), m = 1..NR.
     //    Column (kk, c) is split into `parts` contiguous step ranges, one per thread;
     //    steps where both chunks are real run predicate-free, padding steps (δ = 0,
@@ -713,7 +714,8 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
     for (int c = 0; c < (Q == 0 ? d : 1); ++c) x0[c] = __ldg(xb + (Q == 0 ? c : dig[0]));
     float p10v = 0.f;
     if (P1S && tid < d) p10v = __ldg(xb + seg0 * d + tid) - __ldg(xb + tid);
-    raw = pair_stage_and_table<PF>(xb, seg0, slen, CL, UP, tab, raw, bar);
+    raw = pair_stage_and_table<PF>(xb, seg0, slen, CL, UP, tab, raw, bar,
+                                   (g.phases != nullptr && g.G == 1) ? g.phases + rowid * 10 + 8 : nullptr);
     phase(1);
     // 3. per-thread state: slice `pre` of chunks 2k and 2k+1, started from (1, X[s_j] - X[0], 0, ...)
     f2 st[PF::S];

@@ -56,7 +56,9 @@ for combo in combos:
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1) * 1e3 / (40 if pipelined else 1))
     p = ph.cpu()
-    if plan.segments == 1:
+    staged = None
+    if plan.segments == 1:  # slot 8 holds the end of staging (inside the stage phase)
+        staged = int((p[:, 8] - p[:, 0]).double().median().item())
         p[:, 8] = p[:, 7]
         p[:, 9] = p[:, 7]
     dlt = (p[:, 1:10] - p[:, 0:9]).double().median(dim=0).values.tolist()
@@ -64,6 +66,6 @@ for combo in combos:
     rec = {"cfg": name, "B": B, "L": L, "G": st.segments, "U": st.chunks, "CL": st.fold_steps,
            "kernel_us": round(min(res), 2), "phase_cycles": dict(zip(names, [int(x) for x in dlt])),
            "total_cycles": int((p[:, 9] - p[:, 0]).double().median().item()),
-           "seg_combine_max": int((p[:, 9] - p[:, 8]).max().item()),
+           "seg_combine_max": int((p[:, 9] - p[:, 8]).max().item()), "staging_done_at": staged,
            "start_spread_cycles": int((start.max() - start.min()).item())}
     print(json.dumps(rec), flush=True)

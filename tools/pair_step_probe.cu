@@ -232,9 +232,10 @@ void run(const char* name, float* sink) {
         cudaEventSynchronize(e1);
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
-        const double pipe = 2.0 * threads * (double)steps * 45 / 32.0;  // lean-equivalent warp-pipe cycles per SM
+        cudaGetLastError();
+        const double pipe = 2.0 * threads * (double)steps * F::ops_per_step() / 32.0;  // executed warp-pipe cycles per SM
         const double util = pipe / 4.0 / (ms * 1e-3 * clk * 1e3);
-        printf("%s warps/SMSP=%.2f threads=%d  lean-equiv FMA-pipe util (at max clk)=%.3f  (%.2f ms) %s\n", name, threads / 128.0,
+        printf("%s warps/SMSP=%.2f threads=%d  executed FMA-pipe util (at max clk)=%.3f  (%.2f ms) %s\n", name, threads / 128.0,
                threads, util, ms, cudaGetErrorString(cudaGetLastError()));
     }
 }
@@ -242,9 +243,11 @@ void run(const char* name, float* sink) {
 int main() {
     float* sink;
     cudaMalloc(&sink, 148 * 1024 * sizeof(float));
-    run<5, 4, 2, 1, 0>("d5N4Q2 lean plain   ", sink);
-    run<5, 4, 2, 2, 0>("d5N4Q2 pos plain    ", sink);
-    run<5, 4, 2, 2, 1>("d5N4Q2 pos prefetch ", sink);
-    run<5, 4, 2, 2, 2>("d5N4Q2 pos regs     ", sink);
+    run<5, 4, 2, 1, 2>("d5N4Q2 lean regs    ", sink);
+    run<5, 4, 2, 1, 1>("d5N4Q2 lean prefetch", sink);
+    run<4, 4, 2, 1, 2>("d4N4Q2 lean regs    ", sink);
+    run<4, 4, 2, 1, 1>("d4N4Q2 lean prefetch", sink);
+    run<6, 3, 1, 1, 2>("d6N3Q1 lean regs    ", sink);
+    run<8, 3, 2, 1, 2>("d8N3Q2 lean regs    ", sink);
     return 0;
 }
