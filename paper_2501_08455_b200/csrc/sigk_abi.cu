@@ -746,13 +746,24 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
         if (plan.v && plan.v->stream_launch) {
             const bool overlap = !(tun && tun->no_overlap) &&
                                  may_overlap_previous(dev, s, X, sizeof(Real) * B * L * d, out, sizeof(Real) * B * M * D);
-            e = plan.v->stream_launch(X, B, L, plan.U, out, s, overlap);
+            // one CTA per path: when the batch leaves SMs idle, the widest
+            // chunking that fits keeps more warps per SM on the copy-out
+            // (C2: U 10 -> 20, 102 -> 88 µs)
+            int U = plan.U;
+            if (!(tun && tun->chunks > 0) && B <= device_info(dev).sms)
+                U = std::max(U, (int)std::min<int64_t>(2 * plan.v->pair_units_max, std::max<int64_t>(2, M / 8)));
+            for (;;) {
+                e = plan.v->stream_launch(X, B, L, U, out, s, overlap);
+                if (e != cudaErrorInvalidValue || U <= plan.U) break;
+                cudaGetLastError();
+                U = std::max(plan.U, U - 2);
+            }
             if (e == cudaSuccess) {
                 done = true;
                 local.family = SIGK_FAMILY_PAIR;
                 local.prefix_len = plan.v->Q;
                 local.threads_per_unit = plan.v->P;
-                local.chunks = std::max(2, plan.U / 2 * 2);
+                local.chunks = std::max(2, U / 2 * 2);
                 local.fold_steps = (M + local.chunks - 1) / local.chunks;
             } else if (e != cudaErrorInvalidValue) {
                 return cuda_fail(e, "stream launch");
