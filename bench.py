@@ -116,6 +116,27 @@ class ClockSampler:
         return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
 
 
+def bind_to_gpu_numa(index):
+    """Run on the host cores local to the GPU (NVML CPU affinity) so pinned
+    host buffers are first-touched on the GPU's NUMA node: the e2e copies then
+    avoid the socket interconnect."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            full = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, cpus)
+            return full
+    except Exception:
+        pass
+    return None
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -188,6 +209,7 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    all_cores = bind_to_gpu_numa(torch.cuda.current_device())  # restored for the CPU baseline
     if world > 1:
         import torch.distributed as dist
 
@@ -325,6 +347,8 @@ def run_ours(args):
         parity = max(float(np.abs(got[:, off[n]:off[n + 1]] - ref[:, off[n]:off[n + 1]]).max()
                          / np.abs(ref[:, off[n]:off[n + 1]]).max()) for n in range(N))
 
+    if all_cores:
+        os.sched_setaffinity(0, all_cores)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(pool[0].cpu().numpy(), N)
