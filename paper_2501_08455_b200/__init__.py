@@ -279,12 +279,12 @@ def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: Exe
 
 
 def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
-                     stats: KernelStats | None = None, *, out=None, family: int = 0):
+                     stats: KernelStats | None = None, *, out=None, family: int = 0, chunks: int = 0):
     """Reference ``sigkit::signature_stream`` (kernels.cpp:156-198): (B, L, d) -> (B, L-1, D),
     row (b, t) = signature of X[b, 0..t+1]. L < 2 raises DomainError."""
     select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
     st = _Stats()
-    tun = _Tuning(family=family)
+    tun = _Tuning(family=family, chunks=chunks)
     if _is_torch(paths):
         import torch
 
@@ -317,11 +317,13 @@ def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, ca
 
 
 def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.Auto,
-                  caps: ExecutionCaps | None = None, stats: KernelStats | None = None):
+                  caps: ExecutionCaps | None = None, stats: KernelStats | None = None, *, chunks: int = 0):
     """Reference ``sigkit::signature_vjp`` (autodiff.cpp:218-224): d<cotangent, Sig(X)>/dX,
-    (B, L, d), for a (B, D) cotangent. numpy in -> numpy out; CUDA tensors in -> CUDA tensor out."""
+    (B, L, d), for a (B, D) cotangent. numpy in -> numpy out; CUDA tensors in -> CUDA tensor out.
+    ``chunks`` pins the number of backward chunks per path (0: planned; 1: one sequential walk)."""
     select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
     st = _Stats()
+    tun = C.byref(_Tuning(chunks=chunks)) if chunks else None
     if _is_torch(paths):
         import torch
 
@@ -334,7 +336,7 @@ def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.
         fn = lib().sigk_signature_vjp_f32 if X.dtype == torch.float32 else lib().sigk_signature_vjp_f64
         with torch.cuda.device(X.device):
             s = torch.cuda.current_stream(X.device).cuda_stream
-            _check(fn(X.data_ptr(), B, L, d, depth, cot.data_ptr(), grad.data_ptr(), SIGK_X_ON_DEVICE, s, None,
+            _check(fn(X.data_ptr(), B, L, d, depth, cot.data_ptr(), grad.data_ptr(), SIGK_X_ON_DEVICE, s, tun,
                       C.byref(st)))
     else:
         X = np.asarray(paths)
@@ -347,7 +349,7 @@ def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.
             raise DomainError("signature_vjp: cotangent shape does not match paths/depth")
         grad = np.empty_like(X)
         fn = lib().sigk_signature_vjp_f32 if X.dtype == np.float32 else lib().sigk_signature_vjp_f64
-        _check(fn(X.ctypes.data, B, L, d, depth, cot.ctypes.data, grad.ctypes.data, 0, None, None, C.byref(st)))
+        _check(fn(X.ctypes.data, B, L, d, depth, cot.ctypes.data, grad.ctypes.data, 0, None, tun, C.byref(st)))
     if stats is not None:
         for f, _ in _Stats._fields_:
             setattr(stats, f, getattr(st, f))

@@ -99,3 +99,12 @@ def test_stream_device_tensors(sk):
     torch.cuda.synchronize()
     assert tuple(out.shape) == (32, 399, 780)
     assert max(errs(out.cpu().numpy(), oracle_stream(X.cpu().numpy(), 4), 5, 4)) <= F32_TOL
+
+
+@pytest.mark.parametrize("chunks", [2, 6, 20])
+def test_stream_chunk_counts(sk, chunks):
+    X = brownian(4, 257, 5, seed=31)
+    st = sk.KernelStats()
+    got = sk.signature_stream(X, 4, stats=st, chunks=chunks)
+    assert st.chunks == chunks, st
+    assert max(errs(got, oracle_stream(X, 4), 5, 4)) <= F32_TOL

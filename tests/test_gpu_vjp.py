@@ -83,3 +83,17 @@ def test_vjp_shape_errors(sk):
         sk.signature_vjp(np.zeros((2, 5, 3)), 3, np.zeros((2, 38)))
     with pytest.raises(sk.DomainError):
         sk.signature_vjp(np.zeros((2, 5, 3)), 0, np.zeros((2, 39)))
+
+
+@pytest.mark.parametrize("chunks", [2, 3, 7])
+def test_vjp_chunked_matches_single_walk(sk, chunks):
+    # boundary cotangents through chunk signatures == one sequential backward walk
+    X = walk(3, 101, 3, seed=21)
+    cot = np.random.default_rng(22).standard_normal((3, sk.sig_dim(3, 4)))
+    st = sk.KernelStats()
+    one = sk.signature_vjp(X, 4, cot, chunks=1, stats=st)
+    assert st.chunks == 1
+    got = sk.signature_vjp(X, 4, cot, chunks=chunks, stats=st)
+    assert st.chunks == chunks
+    assert rel(got, one) <= 1e-11
+    assert rel(got, O.ref_vjp(X, 4, cot)) <= 1e-10
