@@ -63,6 +63,15 @@ extern "C" {
  * the legacy default stream) and touches no host memory. */
 #define SIGK_X_ON_DEVICE 1u
 #define SIGK_OUT_ON_DEVICE 2u
+/* Host buffers, asynchronous (sigk_signature_f32/_f64 only): X and out must be
+ * page-locked (cudaHostAlloc / cudaHostRegister). The call enqueues H2D,
+ * kernels and D2H and returns; the result is in `out` once `stream` is
+ * synchronised. X must hold its data at call time (no device work still
+ * writing it) and stay untouched until the stream is synchronised. Consecutive calls on
+ * one stream rotate over a ring of device staging slots with their own copy
+ * streams, so the H2D of call i+1 overlaps the kernels and D2H of call i
+ * (throughput bound by PCIe, not by the sum of the three). */
+#define SIGK_ASYNC_HOST 4u
 
 /* Structural counters (the reference KernelStats, kernels.hpp:86-91, plus
  * the GPU decomposition). fold_steps = increments folded by each (path,

@@ -27,7 +27,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SIGK_LIB_PATH") or os.path.join(_HERE, "libsigk.so")
 
 SIGK_OK, SIGK_EDOMAIN, SIGK_ERESOURCE, SIGK_EDEVICE, SIGK_ETRAINING = 0, 1, 2, 3, 4
-SIGK_X_ON_DEVICE, SIGK_OUT_ON_DEVICE = 1, 2
+SIGK_X_ON_DEVICE, SIGK_OUT_ON_DEVICE, SIGK_ASYNC_HOST = 1, 2, 4
 
 
 class DomainError(ValueError):
@@ -232,16 +232,30 @@ def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_ge
     if _is_torch(paths):
         import torch
 
-        if not paths.is_cuda:
-            raise DomainError("torch input must be a CUDA tensor (use numpy for host buffers)")
         B, L, d = _validate_shape(paths.shape, depth)
         if paths.dtype not in (torch.float32, torch.float64):
             raise DomainError(f"unsupported dtype {paths.dtype}")
-        X = paths.contiguous()
+        fn = lib().sigk_signature_f32 if paths.dtype == torch.float32 else lib().sigk_signature_f64
         D = sig_dim(d, depth)
+        if not paths.is_cuda:
+            # page-locked host tensors: asynchronous host mode on the current CUDA
+            # stream (SIGK_ASYNC_HOST); `out` is valid once that stream is synchronised
+            if not paths.is_pinned():
+                raise DomainError("torch CPU input must be pinned (async host mode); use numpy for plain host buffers")
+            X = paths if paths.is_contiguous() else paths.contiguous().pin_memory()
+            if out is None:
+                out = torch.empty((B, D), dtype=X.dtype, pin_memory=True)
+            if out.is_cuda or not out.is_pinned():
+                raise DomainError("async host mode needs a pinned CPU `out`")
+            s = torch.cuda.current_stream().cuda_stream
+            _check(fn(X.data_ptr(), B, L, d, depth, out.data_ptr(), SIGK_ASYNC_HOST, s, C.byref(tun), C.byref(st)))
+            if stats is not None:
+                for f, _ in _Stats._fields_:
+                    setattr(stats, f, getattr(st, f))
+            return out
+        X = paths.contiguous()
         if out is None:
             out = torch.empty((B, D), dtype=X.dtype, device=X.device)
-        fn = lib().sigk_signature_f32 if X.dtype == torch.float32 else lib().sigk_signature_f64
         with torch.cuda.device(X.device):
             s = torch.cuda.current_stream(X.device).cuda_stream
             _check(fn(X.data_ptr(), B, L, d, depth, out.data_ptr(), SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE,
@@ -470,5 +484,5 @@ __all__ = [
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
     "signature_stream", "signature_vjp", "TrainConfig", "train", "increments", "scaled_increments",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
-    "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES",
+    "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES", "SIGK_X_ON_DEVICE", "SIGK_OUT_ON_DEVICE", "SIGK_ASYNC_HOST",
 ]

@@ -552,6 +552,42 @@ struct Staging {
     cudaEvent_t ev[2 * kPieces + 2] = {};
 };
 
+// Asynchronous host-buffer calls (SIGK_ASYNC_HOST): a ring of staging slots
+// per (device, stream). Slot k serves calls k, k+R, ...; before reusing it a
+// call waits (on the device, never the host) for the kernel that read its X
+// and the D2H that drained its output. Copies and kernels run on the ring's
+// own streams; the caller's stream only waits for each call's D2H, so
+// synchronising it covers the results without serialising the next call.
+struct AsyncRing {
+    static constexpr int R = 3;
+    std::mutex mu;
+    void* p[R] = {};
+    size_t n[R] = {};
+    cudaStream_t hs = nullptr, cs = nullptr, ds = nullptr;  // H2D, kernels, D2H
+    cudaEvent_t h2d[R] = {}, kdone[R] = {}, d2h[R] = {};
+    bool used[R] = {};
+    unsigned next = 0;
+};
+
+static AsyncRing& ring_for(int dev, cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, cudaStream_t>, AsyncRing*>> tab;
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& kv : tab)
+        if (kv.first.first == dev && kv.first.second == s) return *kv.second;
+    tab.emplace_back(std::make_pair(dev, s), new AsyncRing());
+    return *tab.back().second;
+}
+
+static bool is_pinned_host(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 // Host-buffer staging per (device, stream); entries live for the process.
 static Staging& staging_for(int dev, cudaStream_t s) {
     static std::mutex mu;
@@ -584,6 +620,62 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
             if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
         }
         return rc;
+    }
+    if (flags & SIGK_ASYNC_HOST) {
+        if (xdev || odev) return fail(SIGK_EDOMAIN, "SIGK_ASYNC_HOST is for host X and out");
+        if (!is_pinned_host(X) || !is_pinned_host(out))
+            return fail(SIGK_EDOMAIN, "SIGK_ASYNC_HOST needs page-locked X and out (cudaHostAlloc/cudaHostRegister)");
+        int dev = 0;
+        cudaGetDevice(&dev);
+        AsyncRing& rg = ring_for(dev, s);
+        std::lock_guard<std::mutex> lock(rg.mu);
+        if (!rg.hs) {
+            cudaStreamCreateWithFlags(&rg.hs, cudaStreamNonBlocking);
+            cudaStreamCreateWithFlags(&rg.cs, cudaStreamNonBlocking);
+            cudaStreamCreateWithFlags(&rg.ds, cudaStreamNonBlocking);
+            for (int k = 0; k < AsyncRing::R; ++k) {
+                cudaEventCreateWithFlags(&rg.h2d[k], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&rg.kdone[k], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&rg.d2h[k], cudaEventDisableTiming);
+            }
+        }
+        const int k = (int)(rg.next++ % AsyncRing::R);
+        const size_t ooff = (xbytes + 255) / 256 * 256, need = ooff + obytes;
+        if (rg.n[k] < need) {
+            if (rg.p[k]) {
+                cudaEventSynchronize(rg.kdone[k]);  // growth is rare: let the slot drain first
+                cudaEventSynchronize(rg.d2h[k]);
+                cudaFree(rg.p[k]);
+            }
+            rg.p[k] = nullptr;
+            rg.n[k] = 0;
+            e = cudaMalloc(&rg.p[k], need);
+            if (e != cudaSuccess) return cuda_fail(e, "async staging allocation");
+            rg.n[k] = need;
+            rg.used[k] = false;
+        }
+        Real* xbuf = static_cast<Real*>(rg.p[k]);
+        Real* obuf = reinterpret_cast<Real*>(static_cast<char*>(rg.p[k]) + ooff);
+        // H2D on the copy stream, ordered only after the slot's last reader: X is
+        // host data that is complete at call time, so it need not wait for the
+        // caller's queued work (that would serialise consecutive calls)
+        if (rg.used[k]) cudaStreamWaitEvent(rg.hs, rg.kdone[k], 0);
+        e = cudaMemcpyAsync(xbuf, X, xbytes, cudaMemcpyHostToDevice, rg.hs);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+        cudaEventRecord(rg.h2d[k], rg.hs);
+        cudaStreamWaitEvent(rg.cs, rg.h2d[k], 0);
+        if (rg.used[k]) cudaStreamWaitEvent(rg.cs, rg.d2h[k], 0);  // obuf drained
+        rc = run_device<Real>(xbuf, (int64_t)B, (int64_t)L, d, N, obuf, rg.cs, tun, st);
+        if (rc != SIGK_OK) return rc;
+        cudaEventRecord(rg.kdone[k], rg.cs);
+        cudaStreamWaitEvent(rg.ds, rg.kdone[k], 0);
+        e = cudaMemcpyAsync(out, obuf, obytes, cudaMemcpyDeviceToHost, rg.ds);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+        cudaEventRecord(rg.d2h[k], rg.ds);
+        cudaStreamWaitEvent(s, rg.d2h[k], 0);  // synchronising the caller's stream covers the result
+        rg.used[k] = true;
+        e = cudaPeekAtLastError();
+        return e == cudaSuccess ? SIGK_OK : cuda_fail(e, "async host call");
     }
     // Host buffers: the call is synchronous. Device staging comes from a
     // per-(device, stream) buffer that persists across calls (a stream-ordered
