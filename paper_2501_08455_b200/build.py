@@ -36,6 +36,8 @@ def _units():
         for d in DIMS:
             units.append((f"variants_{real}_d{d}", os.path.join(CSRC, "variants_inst.cu"),
                           [f"-DSIGK_REAL={real}", f"-DSIGK_DIM={d}"]))
+    units.append(("vjp_f32", os.path.join(CSRC, "vjp_inst.cu"), ["-DSIGK_VJP_REAL_F32=1"]))
+    units.append(("vjp_f64", os.path.join(CSRC, "vjp_inst.cu"), ["-DSIGK_VJP_REAL_F32=0"]))
     units.append(("sigkit_api", os.path.join(CSRC, "sigkit_api.cpp"), []))
     units.append(("bench_api", os.path.join(CSRC, "bench_api.cpp"), []))
     units.append(("model_api", os.path.join(CSRC, "model_api.cpp"), []))

@@ -1010,7 +1010,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         release();
         return cuda_fail(e, "vjp allocation");
     }
-    const size_t work = sizeof(Real) * vjp_work_elems(D, d);
+    const size_t work = sizeof(Real) * vjp_work_elems(D, d, N);
     const int use_smem = work <= 160 * 1024;
     Real* gwork = nullptr;
     if (!use_smem) {
@@ -1019,9 +1019,11 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             release();
             return cuda_fail(e, "vjp work allocation");
         }
-    } else if (work > 48 * 1024) {
-        cudaFuncSetAttribute(vjp_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)work);
     }
+    VjpKernelFn<Real> vk;
+    if constexpr (sizeof(Real) == 4) vk = vjp_kernel_for_f32(d, N);
+    else vk = vjp_kernel_for_f64(d, N);
+    if (use_smem && work > 48 * 1024) cudaFuncSetAttribute(vk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)work);
     if (M > 0) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(B * U));
@@ -1036,7 +1038,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;  // the kernel waits for its predecessor before reading anything
-        e = cudaLaunchKernelEx(&cfg, vjp_kernel<Real>, X, L, d, N, D, static_cast<const Real*>(states), cbars, U, CL,
+        e = cudaLaunchKernelEx(&cfg, vk, X, L, d, N, D, static_cast<const Real*>(states), cbars, U, CL,
                                dbar, gwork, use_smem);
         if (e != cudaSuccess) {
             release();

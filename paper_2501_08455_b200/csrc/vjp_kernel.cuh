@@ -29,7 +29,14 @@ __device__ __forceinline__ Real warp_sum(Real v) {
 // Reals (shared memory when it fits, else `gwork` + blockIdx * that). The
 // state row of the next step is prefetched with cp.async into a second
 // buffer while the current step computes.
-__host__ __device__ constexpr int64_t vjp_work_elems(int64_t D, int d) { return 6 * D + 3 * d + 4; }
+__host__ __device__ constexpr int64_t vjp_horner_elems(int d, int N) {
+    int64_t p = 1;
+    for (int n = 1; n < N; ++n) p *= d;
+    return N > 2 ? 2 * (N - 2) * p : 0;  // Ā Horner chains: two buffers of d^(N-1) per target n < N-1
+}
+__host__ __device__ constexpr int64_t vjp_work_elems(int64_t D, int d, int N) {
+    return 6 * D + 3 * d + 4 + vjp_horner_elems(d, N);
+}
 
 template <typename Real>
 __device__ __forceinline__ void prefetch_row(Real* dst, const Real* src, int64_t n) {
@@ -49,19 +56,23 @@ __device__ __forceinline__ void prefetch_row(Real* dst, const Real* src, int64_t
 // path b backwards, starting from the cotangent of the state at the chunk's
 // end (cbars row b*U + j; the boundary kernel below), and writes δ̄_s of its
 // steps to dbar (B, M, d); vjp_grad_kernel turns those into ∂/∂X.
-template <typename Real>
-__global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, int64_t L, int d, int N, int64_t D,
+template <typename Real, int DD = 0, int NN = 0>
+__global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, int64_t L, int d_, int N_, int64_t D,
                                                   const Real* __restrict__ states, const Real* __restrict__ cbars,
                                                   int U, int64_t CL, Real* __restrict__ dbar,
                                                   Real* __restrict__ gwork, int use_smem) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // DD/NN > 0: compile-time shape (loops unroll, offsets fold); 0: runtime
+    const int d = DD > 0 ? DD : d_;
+    const int N = NN > 0 ? NN : N_;
     __shared__ int64_t off[kGenericMaxDepth + 1];
+    auto OFF = [&](int n) -> int { return (int)off[n]; };
     __shared__ Real invfact[kGenericMaxDepth + 1];
     const int64_t b = blockIdx.x / U, j = blockIdx.x - (blockIdx.x / U) * U;
     const int64_t M = L - 1;
     const int64_t s_lo = j * CL < M ? j * CL : M, s_hi = (j + 1) * CL < M ? (j + 1) * CL : M;
     const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
-    Real* work = use_smem ? reinterpret_cast<Real*>(smem_raw) : gwork + (int64_t)blockIdx.x * vjp_work_elems(D, d);
+    Real* work = use_smem ? reinterpret_cast<Real*>(smem_raw) : gwork + (int64_t)blockIdx.x * vjp_work_elems(D, d, N);
     Real* cbar = work;            // [D] cotangent of the state after the step
     Real* abar = cbar + D;        // [D] ... of the state before it
     Real* ebar = abar + D;        // [D] ... of exp(δ)
@@ -70,11 +81,13 @@ __global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, in
     Real* dl = E + 3 * D;         // [d] δ
     Real* db = dl + d;            // [d] δ̄ of this step
     Real* dbn = db + d;           // [d] δ̄ of the next step
+    Real* gh = dbn + d + 4;       // [N-2][2][d^(N-1)] Ā Horner chains
     if (tid == 0) {
         off[0] = 0;
         int64_t p = 1;
         Real f = 1;
         invfact[0] = 1;
+#pragma unroll
         for (int n = 1; n <= N; ++n) {
             p *= d;
             off[n] = off[n - 1] + p;
@@ -109,90 +122,92 @@ __global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, in
         }
         __syncthreads();
         // E_n[P d + c] = E_{n-1}[P] δ[c] / n, levels ascending
+#pragma unroll
         for (int n = 1; n <= N; ++n) {
-            const int psz = n == 1 ? 1 : (int)(off[n - 1] - off[n - 2]);  // d^(n-1)
+            const int psz = n == 1 ? 1 : (int)(OFF(n - 1) - OFF(n - 2));  // d^(n-1)
             const Real inv = Real(1) / Real(n);
             for (int P = tid; P < psz; P += nth) {
-                const Real e = (n == 1 ? Real(1) : E[off[n - 2] + P]) * inv;
-                Real* dst = E + off[n - 1] + (int64_t)P * d;
+                const Real e = (n == 1 ? Real(1) : E[OFF(n - 2) + P]) * inv;
+                Real* dst = E + OFF(n - 1) + P * d;
                 for (int c = 0; c < d; ++c) dst[c] = e * dl[c];
             }
             __syncthreads();
         }
-        // Ā_n[I] = C̄_n[I] + Σ_j Σ_J C̄_{n+j}[I J] E_j[J],  Ē_n[J] = C̄_n[J] + Σ_i Σ_I C̄_{i+n}[I J] A_i[I]
-        // (level by level; long dot products by a whole warp, short ones by a thread)
+        // Ā_n[I] = C̄_n[I] + Σ_j Σ_J C̄_{n+j}[I J] E_j[J] by Horner over the trailing
+        // index, all targets n at once, one stage per level m (descending):
+        //   G_{n,m}[I] = C̄_m[I] + Σ_c G_{n,m+1}[I c] δ[c] / (m-n+1),  G_{n,N} = C̄_N,  Ā_n = G_{n,n}
+        // (d FMAs per output, every output of a stage in parallel)
+        if (A != nullptr) {
+            const int dN1 = OFF(N - 1) - OFF(N - 2);  // d^(N-1)
+            int cur = 0;
+            for (int m = N - 1; m >= 1; --m) {
+                const int szm = OFF(m) - OFF(m - 1), om = OFF(m - 1);
+                for (int item = tid; item < m * szm; item += nth) {
+                    const int n = 1 + item / szm, I = item - (item / szm) * szm;
+                    const Real* src = (m + 1 == N) ? cbar + OFF(N - 1) + I * d
+                                                   : gh + ((n - 1) * 2 + (cur ^ 1)) * dN1 + I * d;
+                    Real acc = Real(0);
+#pragma unroll
+                    for (int c = 0; c < (DD > 0 ? DD : d); ++c) acc = fma(src[c], dl[c], acc);
+                    const Real v = fma(acc, Real(1) / Real(m - n + 1), cbar[om + I]);
+                    if (n == m) abar[om + I] = v;
+                    else gh[((n - 1) * 2 + cur) * dN1 + I] = v;
+                }
+                __syncthreads();
+                cur ^= 1;
+            }
+        }
+        // Ē_n[J] = C̄_n[J] + Σ_i Σ_I C̄_{i+n}[I J] A_i[I] (leading-index contractions:
+        // long dot products by a whole warp, short ones by a thread)
         for (int n = 1; n <= N; ++n) {
-            const int sz = (int)(off[n] - off[n - 1]);
-            const int on = (int)off[n - 1];
-            const int len = (int)(off[N - n] - 0);  // Σ_{j=1}^{N-n} d^j
+            const int sz = (int)(OFF(n) - OFF(n - 1));
+            const int on = (int)OFF(n - 1);
+            const int len = (int)(OFF(N - n) - 0);  // Σ_{i=1}^{N-n} d^i
             if (A == nullptr || n == N) {
                 for (int i = tid; i < sz; i += nth) {
-                    abar[on + i] = cbar[on + i];
+                    if (A == nullptr || n == N) abar[on + i] = cbar[on + i];
                     ebar[on + i] = cbar[on + i];
                 }
             } else if (len >= 64) {
-                for (int item = warp; item < 2 * sz; item += nw) {
-                    const bool is_a = item < sz;
-                    const int I = is_a ? item : item - sz;
+                for (int I = warp; I < sz; I += nw) {
                     Real acc = Real(0);
-                    if (is_a) {
-                        int w = 1;
-                        for (int j = 1; n + j <= N; ++j) {
-                            w *= d;
-                            const Real* cr = cbar + off[n + j - 1] + (int64_t)I * w;
-                            const Real* er = E + off[j - 1];
-                            for (int J = lane; J < w; J += 32) acc = fma(cr[J], er[J], acc);
-                        }
-                    } else {
-                        for (int i = 1; i + n <= N; ++i) {
-                            const int wi = (int)(off[i] - off[i - 1]);
-                            const Real* cr = cbar + off[i + n - 1] + I;
-                            const Real* ar = A + off[i - 1];
-                            for (int P = lane; P < wi; P += 32) acc = fma(cr[(int64_t)P * sz], ar[P], acc);
-                        }
+                    for (int i = 1; i + n <= N; ++i) {
+                        const int wi = (int)(OFF(i) - OFF(i - 1));
+                        const Real* cr = cbar + OFF(i + n - 1) + I;
+                        const Real* ar = A + OFF(i - 1);
+                        for (int P = lane; P < wi; P += 32) acc = fma(cr[P * sz], ar[P], acc);
                     }
                     acc = warp_sum(acc);
-                    if (lane == 0) (is_a ? abar : ebar)[on + I] = cbar[on + I] + acc;
+                    if (lane == 0) ebar[on + I] = cbar[on + I] + acc;
                 }
             } else {
-                for (int item = tid; item < 2 * sz; item += nth) {
-                    const bool is_a = item < sz;
-                    const int I = is_a ? item : item - sz;
+                for (int I = tid; I < sz; I += nth) {
                     Real acc = cbar[on + I];
-                    if (is_a) {
-                        int w = 1;
-                        for (int j = 1; n + j <= N; ++j) {
-                            w *= d;
-                            const Real* cr = cbar + off[n + j - 1] + (int64_t)I * w;
-                            const Real* er = E + off[j - 1];
-                            for (int J = 0; J < w; ++J) acc = fma(cr[J], er[J], acc);
-                        }
-                    } else {
-                        for (int i = 1; i + n <= N; ++i) {
-                            const int wi = (int)(off[i] - off[i - 1]);
-                            const Real* cr = cbar + off[i + n - 1] + I;
-                            const Real* ar = A + off[i - 1];
-                            for (int P = 0; P < wi; ++P) acc = fma(cr[(int64_t)P * sz], ar[P], acc);
-                        }
+                    for (int i = 1; i + n <= N; ++i) {
+                        const int wi = (int)(OFF(i) - OFF(i - 1));
+                        const Real* cr = cbar + OFF(i + n - 1) + I;
+                        const Real* ar = A + OFF(i - 1);
+                        for (int P = 0; P < wi; ++P) acc = fma(cr[P * sz], ar[P], acc);
                     }
-                    (is_a ? abar : ebar)[on + I] = acc;
+                    ebar[on + I] = acc;
                 }
             }
         }
         __syncthreads();
         // e_n = e_{n-1} ⊗ δ / n, top degree down (autodiff.cpp:86-98)
+#pragma unroll
         for (int n = N; n >= 2; --n) {
-            const int psz = (int)(off[n - 1] - off[n - 2]);
+            const int psz = (int)(OFF(n - 1) - OFF(n - 2));
             const Real inv = Real(1) / Real(n);
-            const Real* en = ebar + off[n - 1];
+            const Real* en = ebar + OFF(n - 1);
             for (int P = tid; P < psz; P += nth) {
                 Real acc = Real(0);
                 for (int c = 0; c < d; ++c) acc = fma(en[P * d + c], dl[c], acc);
-                ebar[off[n - 2] + P] = fma(acc, inv, ebar[off[n - 2] + P]);
+                ebar[OFF(n - 2) + P] = fma(acc, inv, ebar[OFF(n - 2) + P]);
             }
             for (int c = warp; c < d; c += nw) {
                 Real acc = Real(0);
-                for (int P = lane; P < psz; P += 32) acc = fma(en[P * d + c], E[off[n - 2] + P], acc);
+                for (int P = lane; P < psz; P += 32) acc = fma(en[P * d + c], E[OFF(n - 2) + P], acc);
                 acc = warp_sum(acc);
                 if (lane == 0) db[c] = fma(acc, inv, db[c]);
             }
@@ -205,6 +220,13 @@ __global__ void __launch_bounds__(256) vjp_kernel(const Real* __restrict__ X, in
         __syncthreads();
     }
 }
+
+template <typename Real>
+using VjpKernelFn = void (*)(const Real*, int64_t, int, int, int64_t, const Real*, const Real*, int, int64_t, Real*,
+                             Real*, int);
+// compile-time (d, N) instantiations (csrc/vjp_inst.cu); the runtime kernel otherwise
+VjpKernelFn<float> vjp_kernel_for_f32(int d, int N);
+VjpKernelFn<double> vjp_kernel_for_f64(int d, int N);
 
 // Xseg (B*U, CL+1, d): chunk j of path b as its own path (the last point is
 // repeated past the end: zero increments, identity factors).
