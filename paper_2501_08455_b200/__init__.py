@@ -293,12 +293,13 @@ def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: Exe
 
 
 def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
-                     stats: KernelStats | None = None, *, out=None, family: int = 0, chunks: int = 0):
+                     stats: KernelStats | None = None, *, out=None, family: int = 0, chunks: int = 0,
+                     segments: int = 0):
     """Reference ``sigkit::signature_stream`` (kernels.cpp:156-198): (B, L, d) -> (B, L-1, D),
     row (b, t) = signature of X[b, 0..t+1]. L < 2 raises DomainError."""
     select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
     st = _Stats()
-    tun = _Tuning(family=family, chunks=chunks)
+    tun = _Tuning(family=family, chunks=chunks, segments=segments)
     if _is_torch(paths):
         import torch
 

@@ -841,11 +841,55 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
             // one CTA per path: when the batch leaves SMs idle, the widest
             // chunking that fits keeps more warps per SM on the copy-out
             // (C2: U 10 -> 20, 102 -> 88 µs)
+            const int sms = device_info(dev).sms;
+            // segments per path: one CTA per path leaves SMs idle for small
+            // batches, so split each path into G pieces started from their
+            // true prefixes (the pair kernel's segment rows, scanned by
+            // segment_prefix_kernel); >= 64 steps per piece
+            int G = tun && tun->segments > 0 ? tun->segments : 1;
+            if (!(tun && tun->segments > 0)) {
+                G = (int)std::max<int64_t>(1, std::min<int64_t>(8, sms / B));  // measured: B*G ~ SMs
+                while (G > 1 && M / G < 64) --G;
+            }
+            G = (int)std::max<int64_t>(1, std::min<int64_t>(G, M));
+            int64_t SL = (M + G - 1) / G;
+            const void* prefix = nullptr;
+            if (G > 1) {
+                sigk_tuning ts = tp;
+                ts.segments = G;
+                ts.chunks = 0;
+                const Plan sp = cached_plan(d, N, false, dev, B, M, D, &ts);
+                if (!sp.v || !sp.v->prefix_launch || sp.G != G) {
+                    G = 1;
+                    SL = M;
+                } else {
+                    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+                    cudaStreamIsCapturing(s, &cap);
+                    const bool capt = cap != cudaStreamCaptureStatusNone;
+                    bool a1 = false, a2 = false, a3 = false, a4 = false;
+                    void* rows = segment_scratch(dev, s, 8, sizeof(float) * B * G * D, capt, &a1);
+                    void* ctr = segment_scratch(dev, s, 1, sizeof(int) * B, capt, &a2);
+                    void* fin = segment_scratch(dev, s, 9, sizeof(float) * B * D, capt, &a3);
+                    void* pre = segment_scratch(dev, s, 10, sizeof(float) * B * G * D, capt, &a4);
+                    if (!rows || !ctr || !fin || !pre) return fail(SIGK_ERESOURCE, "stream segment scratch");
+                    const int CL2 = (int)((SL + sp.U - 1) / sp.U);
+                    PairLaunch a{X, B, L, G, SL, sp.U, CL2, fin, rows, ctr, s, false, nullptr, nullptr, capt, nullptr};
+                    e = sp.v->pair_launch(a);
+                    if (e == cudaSuccess) e = sp.v->prefix_launch(rows, B, G, pre, s);
+                    for (auto q : {std::make_pair(a1, rows), std::make_pair(a3, fin), std::make_pair(a4, pre)})
+                        if (q.first) cudaFreeAsync(q.second, s);
+                    if (a2) cudaFreeAsync(ctr, s);
+                    if (e != cudaSuccess) return cuda_fail(e, "stream segment prefixes");
+                    prefix = pre;
+                    local.launches += 2;
+                    local.segments = G;
+                }
+            }
             int U = plan.U;
-            if (!(tun && tun->chunks > 0) && B <= device_info(dev).sms)
-                U = std::max(U, (int)std::min<int64_t>(2 * plan.v->pair_units_max, std::max<int64_t>(2, M / 8)));
+            if (!(tun && tun->chunks > 0) && B * G <= sms)
+                U = std::max(U, (int)std::min<int64_t>(2 * plan.v->pair_units_max, std::max<int64_t>(2, SL / 8)));
             for (;;) {
-                e = plan.v->stream_launch(X, B, L, U, out, s, overlap);
+                e = plan.v->stream_launch(X, B, L, U, out, s, overlap || G > 1, G, prefix);
                 if (e != cudaErrorInvalidValue || U <= plan.U) break;
                 cudaGetLastError();
                 U = std::max(plan.U, U - 2);
@@ -856,7 +900,7 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
                 local.prefix_len = plan.v->Q;
                 local.threads_per_unit = plan.v->P;
                 local.chunks = std::max(2, U / 2 * 2);
-                local.fold_steps = (M + local.chunks - 1) / local.chunks;
+                local.fold_steps = (SL + local.chunks - 1) / local.chunks;
             } else if (e != cudaErrorInvalidValue) {
                 return cuda_fail(e, "stream launch");
             }

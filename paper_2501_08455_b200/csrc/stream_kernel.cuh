@@ -100,9 +100,13 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
     constexpr int DL = CLY::DL, LN = CLY::LN, LNP = CLY::LNP, FJ = PF::FJ;
     extern __shared__ __align__(16) unsigned char smem_raw[];
 
-    const int64_t b = blockIdx.x;
+    // CTA (b, sg): steps [sg*SL, (sg+1)*SL) of path b, started from g.prefix row
+    // (b*G + sg) when the path is split (G > 1)
+    const int64_t b = blockIdx.x / g.G, sg = blockIdx.x - (blockIdx.x / g.G) * g.G;
     const int64_t M = L - 1;
-    const int64_t seg0 = 0, slen = M;
+    const int64_t seg0 = sg * g.SL < M ? sg * g.SL : M;
+    const int64_t slen = (seg0 + g.SL < M ? seg0 + g.SL : M) - seg0;
+    const float* __restrict__ pre0 = g.prefix != nullptr ? g.prefix + (b * g.G + sg) * D : nullptr;
     const int U = g.U, UP = g.UP, CL = g.CL;
     const int tid = threadIdx.x, nth = blockDim.x;
     const float* __restrict__ xb = X + b * L * d;
@@ -154,8 +158,10 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
     // ---- true prefixes P^(j), j = 0..U-1, all levels
     CombineSmem<d, N, P1S> S(reinterpret_cast<float*>(area), U);
     float* top = reinterpret_cast<float*>(area) + CLY::floats(U, 0);  // [U+1][LNP]: P^(j)_N
+    if (pre0 != nullptr) pdl_wait();  // the prefix rows come from the previous launch
     if (active) store_low_levels<PF, 1>(st, k, pre, S.ylow);
-    if (tid < d) S.p10[tid] = 0.f;  // P^(0) = 1 (the whole path is one segment)
+    if (tid < d) S.p10[tid] = __ldg(xb + seg0 * d + tid) - __ldg(xb + tid);  // P^(0)_1 = X[seg0] - X[0] (raw is dead)
+    S.p0 = pre0;                                            // P^(0), levels 2..N-1 (null: zero)
     __syncthreads();
     fused_scan<d, N, P1S>(S, U, tid, nth);
     build_c<d, N, P1S>(S, U, tid, nth);
@@ -181,8 +187,8 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
     }
     __syncthreads();
     for (int F = tid; F < LN; F += nth) {  // exclusive scan over chunks, fixed order
-        float run = 0.f;
-        top[F] = 0.f;
+        float run = pre0 != nullptr ? pre0[DL + F] : 0.f;  // P^(0)_N
+        top[F] = run;
         for (int j = 1; j <= U; ++j) {
             run += top[(size_t)j * LNP + F];
             top[(size_t)j * LNP + F] = run;
@@ -202,7 +208,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
     float* stage = reinterpret_cast<float*>(area);
     const size_t sbuf = (size_t)U * TS * D;
     pdl_wait();  // output writes are ordered after the previous launch
-    float* ob = out + b * M * D;
+    float* ob = out + (b * M + seg0) * D;
     const bool bulk = (D * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
     const int sl = (int)slen;

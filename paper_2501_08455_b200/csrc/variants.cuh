@@ -185,35 +185,51 @@ struct PairVariant {
     static constexpr auto skernel = pair_stream_kernel<DIM, DEPTH, Q, NT, MINB>;
     static std::atomic<uint64_t> ssmem_done;
     static cudaError_t stream_launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s,
-                                     bool overlap) {
+                                     bool overlap, int G, const void* prefix) {
         const int64_t M = L - 1;
+        G = std::max(1, G);
+        const int64_t SL = (M + G - 1) / G;
         U = std::max(2, U / 2 * 2);
-        const int CL = (int)((M + U - 1) / U);
+        const int CL = (int)((SL + U - 1) / U);
         int TS = 8;
         size_t sm = 0;
         for (; TS >= 1; TS /= 2) {
-            sm = stream_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(M), TS);
+            sm = stream_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(SL), TS);
             if (sm <= 227 * 1024) break;
         }
         if (TS < 1) return cudaErrorInvalidValue;
         cudaError_t e = opt_in_smem(skernel, sm, ssmem_done);
         if (e != cudaSuccess) return e;
         PairGeom g{};
-        g.G = 1;
-        g.SL = M;
+        g.G = G;
+        g.SL = SL;
         g.U = U;
         g.UP = U / 2;
         g.CL = CL;
         g.threads = threads(U);
-        g.raw_floats = raw_floats(M);
-        return launch_maybe_overlapped(skernel, dim3((unsigned)B), dim3(g.threads), sm, s, overlap,
+        g.raw_floats = raw_floats(SL);
+        g.prefix = G > 1 ? static_cast<const float*>(prefix) : nullptr;
+        return launch_maybe_overlapped(skernel, dim3((unsigned)(B * G)), dim3(g.threads), sm, s, overlap,
                                        static_cast<const float*>(X), L, g, TS, static_cast<float*>(out));
+    }
+    static constexpr auto pkernel = segment_prefix_kernel<DIM, DEPTH, (DIM > 1 && DEPTH > 1)>;
+    static std::atomic<uint64_t> psmem_done;
+    static cudaError_t prefix_launch(const void* rows, int64_t B, int G, void* prefix, cudaStream_t s) {
+        using CLY = CombineLayout<DIM, DEPTH>;
+        const size_t sm = (CLY::floats(G, 0) + (size_t)G * CLY::LN) * 4;
+        if (sm > 227 * 1024) return cudaErrorInvalidValue;
+        cudaError_t e = opt_in_smem(pkernel, sm, psmem_done);
+        if (e != cudaSuccess) return e;
+        return launch_maybe_overlapped(pkernel, dim3((unsigned)B), dim3(256), sm, s, true,
+                                       static_cast<const float*>(rows), G, static_cast<float*>(prefix));
     }
 };
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::smem_done{0};
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::ssmem_done{0};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::psmem_done{0};
 
 // Smallest Q whose pair state (two chunks) fits ~80 registers, or -1.
 constexpr int pick_q_pair(int d, int N) {
@@ -237,6 +253,7 @@ Variant make_pair_variant() {
     v.pair_occupancy = &V::occupancy;
     v.pair_units_max = V::NT / PF::P;
     v.stream_launch = &V::stream_launch;
+    v.prefix_launch = &V::prefix_launch;
     return v;
 }
 

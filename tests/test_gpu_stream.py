@@ -108,3 +108,13 @@ def test_stream_chunk_counts(sk, chunks):
     got = sk.signature_stream(X, 4, stats=st, chunks=chunks)
     assert st.chunks == chunks, st
     assert max(errs(got, oracle_stream(X, 4), 5, 4)) <= F32_TOL
+
+
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_stream_segments(sk, G):
+    # segmented prefix stream: pieces started from the pair kernel's segment prefixes
+    X = brownian(3, 700, 5, seed=41)
+    st = sk.KernelStats()
+    got = sk.signature_stream(X, 4, stats=st, segments=G)
+    assert st.segments == G, st
+    assert max(errs(got, oracle_stream(X, 4), 5, 4)) <= F32_TOL

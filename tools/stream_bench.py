@@ -19,7 +19,7 @@ X = torch.empty((B, L, d), device="cuda")
 sk.brownian(X)
 out = torch.empty((B, L - 1, D), device="cuda")
 s = torch.cuda.current_stream()
-tun = sk._Tuning(family=fam, chunks=int(os.environ.get("STREAM_CHUNKS", "0")))
+tun = sk._Tuning(family=fam, chunks=int(os.environ.get("STREAM_CHUNKS", "0")), segments=int(os.environ.get("STREAM_SEGMENTS", "0")))
 st = sk._Stats()
 
 
