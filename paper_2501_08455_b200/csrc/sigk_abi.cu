@@ -1068,7 +1068,29 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     if constexpr (sizeof(Real) == 4) vk = vjp_kernel_for_f32(d, N);
     else vk = vjp_kernel_for_f64(d, N);
     if (use_smem && work > 48 * 1024) cudaFuncSetAttribute(vk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)work);
-    if (M > 0) {
+    VjpSlice<Real> sl;
+    if constexpr (sizeof(Real) == 4) sl = vjp_slice_for_f32(d, N);
+    else sl = vjp_slice_for_f64(d, N);
+    if (getenv("SIGK_VJP_ELEMENT")) sl.fn = nullptr;  // experiments: the element-parallel kernel
+    if (M > 0 && sl.fn) {
+        // slice-parallel adjoint: SLOTS (path, chunk) items per warp, 4 warps per CTA
+        const int64_t items = B * U, per_cta = 4 * (int64_t)sl.slots;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)((items + per_cta - 1) / per_cta));
+        cfg.blockDim = dim3(128);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, sl.fn, X, L, items, U, CL, static_cast<const Real*>(states), cbars, dbar);
+        if (e != cudaSuccess) {
+            release();
+            return cuda_fail(e, "vjp slice launch");
+        }
+        launches += 1;
+    } else if (M > 0) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(B * U));
         // most per-step loops are level-sized (d^n items): small blocks keep lanes busy;

@@ -1,7 +1,7 @@
 // Compile-time (d, N) instantiations of the reverse-mode kernel (loops over
 // levels unroll, level offsets fold to constants); shapes outside the list
 // use the runtime-shape kernel.
-#include "vjp_kernel.cuh"
+#include "vjp_slice.cuh"
 
 namespace sigk {
 
@@ -25,10 +25,32 @@ static VjpKernelFn<Real> pick(int d, int N) {
     return vjp_kernel<Real, 0, 0>;
 }
 
+template <typename Real, int DD, int NN>
+static void slice_case(int d, int N, VjpSlice<Real>& out) {
+    constexpr int Q = vjp_slice_q(DD, NN);
+    if constexpr (Q > 0) {
+        if (d == DD && N == NN) {
+            out.fn = vjp_slice_kernel<Real, DD, NN, Q>;
+            out.slots = SliceLayout<DD, NN, Q>::SLOTS;
+        }
+    }
+}
+
+template <typename Real>
+static VjpSlice<Real> pick_slice(int d, int N) {
+    VjpSlice<Real> r;
+#define SIGK_VJP_SLICE(DD, NN) slice_case<Real, DD, NN>(d, N, r);
+    SIGK_VJP_SHAPES(SIGK_VJP_SLICE)
+#undef SIGK_VJP_SLICE
+    return r;
+}
+
 #if SIGK_VJP_REAL_F32
 VjpKernelFn<float> vjp_kernel_for_f32(int d, int N) { return pick<float>(d, N); }
+VjpSlice<float> vjp_slice_for_f32(int d, int N) { return pick_slice<float>(d, N); }
 #else
 VjpKernelFn<double> vjp_kernel_for_f64(int d, int N) { return pick<double>(d, N); }
+VjpSlice<double> vjp_slice_for_f64(int d, int N) { return pick_slice<double>(d, N); }
 #endif
 
 }  // namespace sigk

@@ -228,6 +228,15 @@ using VjpKernelFn = void (*)(const Real*, int64_t, int, int, int64_t, const Real
 VjpKernelFn<float> vjp_kernel_for_f32(int d, int N);
 VjpKernelFn<double> vjp_kernel_for_f64(int d, int N);
 
+// slice-parallel adjoint (vjp_slice.cuh) where a prefix length fits a warp
+template <typename Real>
+struct VjpSlice {
+    void (*fn)(const Real*, int64_t, int64_t, int, int64_t, const Real*, const Real*, Real*) = nullptr;
+    int slots = 0;  // (path, chunk) items per warp
+};
+VjpSlice<float> vjp_slice_for_f32(int d, int N);
+VjpSlice<double> vjp_slice_for_f64(int d, int N);
+
 // Xseg (B*U, CL+1, d): chunk j of path b as its own path (the last point is
 // repeated past the end: zero increments, identity factors).
 template <typename Real>

@@ -1,0 +1,317 @@
+// Reverse mode, slice-parallel (the layout of the forward fold): one warp
+// walks `SLOTS` (path, chunk) items backwards, lane (slot, p) owning the
+// prefix slice p = (p_1..p_Q) of the cotangent C̄ and of the state A:
+// levels n >= Q as the d^(n-Q) entries with that prefix, levels n < Q as the
+// scalars at p_1..p_n. Per step (C = A ⊠ exp(δ)):
+//   δ̄ by reverse-mode through the lane's own Horner chains (each output
+//       element of C is owned by exactly one lane: slices by their lane,
+//       low-level scalars by the lane whose trailing digits are zero), then
+//       one segmented sum of d values over the slot's lanes;
+//   Ā_m = Σ_j C̄_{m+j} · E_j by Horner over the trailing index inside the
+//       slice (m >= Q), continued across lanes by segmented sums for m < Q.
+// Exactly the mathematics of the element-parallel kernel (vjp_kernel.cuh)
+// and of the reference's fold adjoint (autodiff.cpp:31-107), with every
+// contraction along the trailing index in registers: d FMAs per output, no
+// block barriers (only __syncwarp around the per-warp reduction scratch).
+#pragma once
+
+#include "vjp_kernel.cuh"
+
+namespace sigk {
+
+// Prefix length for the slice adjoint: the largest q < N with d^q <= 32 and
+// at most 48 state values per lane; 0 when none (the element-parallel kernel).
+__host__ __device__ constexpr int vjp_slice_q(int d, int N) {
+    int best = 0;
+    for (int q = 1; q < N; ++q) {
+        if (ipow(d, q) > 32) break;
+        int s = q - 1;
+        for (int n = q; n <= N; ++n) s += ipow(d, n - q);
+        if (s <= 48) best = q;
+    }
+    return best;
+}
+
+template <int d, int N, int Q>
+struct SliceLayout {
+    static constexpr int P = ipow(d, Q);
+    static constexpr int SLOTS = 32 / P;
+    static constexpr int NLOW = Q - 1;  // levels 1..Q-1 as scalars
+    __host__ __device__ static constexpr int top_off(int n) {  // slice of level n >= Q
+        int o = NLOW;
+        for (int m = Q; m < n; ++m) o += ipow(d, m - Q);
+        return o;
+    }
+    static constexpr int S = top_off(N + 1);
+    // vector Horner stages k = Q+1..N-1 (sizes d^(k-Q)), flat
+    __host__ __device__ static constexpr int vo(int k) {
+        int o = 0;
+        for (int m = Q + 1; m < k; ++m) o += ipow(d, m - Q);
+        return o;
+    }
+    static constexpr int VS = vo(N) > 0 ? vo(N) : 1;
+    static constexpr int GMAX = ipow(d, N - Q);
+};
+
+template <typename Real, int d, int N, int Q>
+struct SliceRev {
+    using LY = SliceLayout<d, N, Q>;
+    static constexpr int S = LY::S, NLOW = LY::NLOW, VS = LY::VS;
+    __device__ __forceinline__ static Real& sc(Real (&v)[S], int k) { return k < Q ? v[k - 1] : v[NLOW]; }
+    // level n (compile time): forward Horner chain of level n, then its reverse for δ̄
+    template <int n>
+    __device__ __forceinline__ static void levels(Real (&a)[S], Real (&cb)[S], const Real (&dl)[d],
+                                                  const Real (&dp)[Q + 1], Real (&gd)[d], Real (&gk)[Q + 1], int p) {
+        if constexpr (n <= N) {
+
+            Real us[Q + 1], usb[Q + 1];
+            const int kq = n - 1 < Q ? n - 1 : Q;  // scalar chain length for level n
+            if (kq >= 1) {
+                us[1] = dp[1] * (Real(1) / Real(n)) + sc(a, 1);
+#pragma unroll
+                for (int k = 2; k <= Q; ++k)
+                    if (k <= kq) us[k] = us[k - 1] * dp[k] * (Real(1) / Real(n - k + 1)) + sc(a, k);
+            }
+            if (n > Q) {
+                Real uv[VS], ub[VS];
+                // forward vector stages k = Q+1..n-1
+#pragma unroll
+                for (int k = Q + 1; k <= N - 1; ++k) {
+                    if (k <= n - 1) {
+                        const Real inv = Real(1) / Real(n - k + 1);
+#pragma unroll
+                        for (int J = 0; J < ipow(d, k - Q); ++J) {
+                            const Real prev = k == Q + 1 ? us[Q] : uv[LY::vo(k - 1) + J / d];
+                            uv[LY::vo(k) + J] = prev * dl[J % d] * inv + a[LY::top_off(k) + J];
+                        }
+                    }
+                }
+                // output level n: T_n'[J] = A_n[J] + u_{n-1}[J/d] δ[J%d]
+                if (n - 1 > Q) {
+#pragma unroll
+                    for (int J = 0; J < ipow(d, n - 1 - Q); ++J) {
+                        Real acc = Real(0);
+#pragma unroll
+                        for (int c = 0; c < d; ++c) {
+                            const Real cv = cb[LY::top_off(n) + J * d + c];
+                            acc += cv * dl[c];
+                            gd[c] += cv * uv[LY::vo(n - 1) + J];
+                        }
+                        ub[LY::vo(n - 1) + J] = acc;
+                    }
+                    // vector stages backwards k = n-1 .. Q+2
+#pragma unroll
+                    for (int k = N - 1; k >= Q + 2; --k) {
+                        if (k <= n - 1) {
+                            const Real inv = Real(1) / Real(n - k + 1);
+#pragma unroll
+                            for (int J = 0; J < ipow(d, k - 1 - Q); ++J) {
+                                Real acc = Real(0);
+#pragma unroll
+                                for (int c = 0; c < d; ++c) {
+                                    const Real ubv = ub[LY::vo(k) + J * d + c];
+                                    acc += ubv * dl[c];
+                                    gd[c] += inv * ubv * uv[LY::vo(k - 1) + J];
+                                }
+                                ub[LY::vo(k - 1) + J] = inv * acc;
+                            }
+                        }
+                    }
+                    // stage Q+1: u_{Q+1}[c] = u_Q δ[c] / (n-Q) + A_{Q+1}[c]
+                    {
+                        const Real inv = Real(1) / Real(n - Q);
+                        Real acc = Real(0);
+#pragma unroll
+                        for (int c = 0; c < d; ++c) {
+                            acc += ub[LY::vo(Q + 1) + c] * dl[c];
+                            gd[c] += inv * ub[LY::vo(Q + 1) + c] * us[Q];
+                        }
+                        usb[Q] = inv * acc;
+                    }
+                } else {  // n == Q+1: T'[c] = A[c] + u_Q δ[c]
+                    Real acc = Real(0);
+#pragma unroll
+                    for (int c = 0; c < d; ++c) {
+                        const Real cv = cb[LY::top_off(n) + c];
+                        acc += cv * dl[c];
+                        gd[c] += cv * us[Q];
+                    }
+                    usb[Q] = acc;
+                }
+                // scalar chain backwards k = Q..2, then k = 1
+#pragma unroll
+                for (int k = Q; k >= 2; --k) {
+                    const Real inv = Real(1) / Real(n - k + 1);
+                    gk[k] += usb[k] * us[k - 1] * inv;
+                    usb[k - 1] = usb[k] * dp[k] * inv;
+                }
+                gk[1] += usb[1] * (Real(1) / Real(n));
+            } else if (p % ipow(d, Q - n) == 0) {  // scalar output owned by this lane
+                const Real cn = sc(cb, n);
+                if (n == 1) {
+                    gk[1] += cn;
+                } else {
+                    gk[n] += cn * us[n - 1];
+                    usb[n - 1] = cn * dp[n];
+#pragma unroll
+                    for (int k = Q; k >= 2; --k) {
+                        if (k <= n - 1) {
+                            const Real inv = Real(1) / Real(n - k + 1);
+                            gk[k] += usb[k] * us[k - 1] * inv;
+                            usb[k - 1] = usb[k] * dp[k] * inv;
+                        }
+                    }
+                    gk[1] += usb[1] * (Real(1) / Real(n));
+                }
+            }
+
+            levels<n + 1>(a, cb, dl, dp, gd, gk, p);
+        }
+    }
+};
+
+template <typename Real, int d, int N, int Q>
+__global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__ X, int64_t L, int64_t items,
+                                                        int U, int64_t CL, const Real* __restrict__ states,
+                                                        const Real* __restrict__ cbars, Real* __restrict__ dbar) {
+    using LY = SliceLayout<d, N, Q>;
+    constexpr int P = LY::P, SLOTS = LY::SLOTS, S = LY::S, NLOW = LY::NLOW, VS = LY::VS, GMAX = LY::GMAX;
+    constexpr int D = level_off(d, N);
+    __shared__ Real red[4][32][d + 1];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int slot = lane / P, p = lane - (lane / P) * P;
+    const bool lane_on = slot < SLOTS;
+    const int64_t item = ((int64_t)blockIdx.x * 4 + warp) * SLOTS + (lane_on ? slot : 0);
+    const bool valid = lane_on && item < items;
+    const int64_t it = valid ? item : 0;
+    const int64_t b = it / U, j = it - (it / U) * U;
+    const int64_t M = L - 1;
+    const int64_t s_lo = j * CL < M ? j * CL : M, s_hi = (j + 1) * CL < M ? (j + 1) * CL : M;
+    int dg[Q + 1];  // digits p_1..p_Q
+#pragma unroll
+    for (int k = 1; k <= Q; ++k) dg[k] = (p / ipow(d, Q - k)) % d;
+    Real (&rd)[32][d + 1] = red[warp];
+
+    // element offsets of the lane's slice inside a signature row
+    auto row_off = [&](int i) -> int {
+        // i < NLOW: level i+1 scalar at prefix p_1..p_{i+1}; else level n slice entry
+        if (i < NLOW) return level_off(d, i) + p / ipow(d, Q - (i + 1));
+        int n = Q, o = NLOW;
+        while (i >= o + ipow(d, n - Q)) {
+            o += ipow(d, n - Q);
+            ++n;
+        }
+        return level_off(d, n - 1) + p * ipow(d, n - Q) + (i - o);
+    };
+    Real cb[S], a[S], an[S];
+    const Real* crow = cbars + it * D;
+    const Real* xb = X + b * L * d;
+    const Real* sb = states + b * M * D;
+    auto load_state = [&](int64_t s, Real (&dst)[S]) {  // S_s = row s-1; identity (zeros) for s <= 0
+#pragma unroll
+        for (int i = 0; i < S; ++i) dst[i] = (valid && s >= 1 && s <= M) ? __ldg(sb + (s - 1) * D + row_off(i)) : Real(0);
+    };
+    pdl_trigger();
+    pdl_wait();  // cbars and states come from the previous launches
+#pragma unroll
+    for (int i = 0; i < S; ++i) cb[i] = valid ? crow[row_off(i)] : Real(0);
+    // scal(k): A_k / C̄_k at prefix p_1..p_k for k <= Q
+    auto sc = [&](Real (&v)[S], int k) -> Real& { return k < Q ? v[k - 1] : v[NLOW]; };
+    load_state(s_hi - 1, an);
+    for (int64_t st = 0; st < CL; ++st) {
+        const int64_t s = s_hi - 1 - st;
+        const bool on = valid && s >= s_lo;
+#pragma unroll
+        for (int i = 0; i < S; ++i) a[i] = an[i];
+        if (on) load_state(s - 1, an);  // prefetch the next (earlier) state
+        Real dl[d];
+#pragma unroll
+        for (int c = 0; c < d; ++c) dl[c] = on ? xb[(s + 1) * d + c] - xb[s * d + c] : Real(0);
+        Real dp[Q + 1];
+#pragma unroll
+        for (int k = 1; k <= Q; ++k)  // δ[p_k] from memory (a register array indexed by p_k would spill)
+            dp[k] = on ? xb[(s + 1) * d + dg[k]] - xb[s * d + dg[k]] : Real(0);
+        Real gd[d], gk[Q + 1];
+#pragma unroll
+        for (int c = 0; c < d; ++c) gd[c] = Real(0);
+#pragma unroll
+        for (int k = 0; k <= Q; ++k) gk[k] = Real(0);
+        // ---- δ̄: reverse through each level's Horner chain (owned outputs only)
+        SliceRev<Real, d, N, Q>::template levels<1>(a, cb, dl, dp, gd, gk, p);
+        // ---- Ā = C̄ pulled back through ⊠ exp(δ)
+        Real ab[S];
+#pragma unroll
+        for (int J = 0; J < GMAX; ++J) ab[LY::top_off(N) + J] = cb[LY::top_off(N) + J];
+        Real gq[Q + 1];  // G_Q of the targets m < Q (scalar per lane)
+#pragma unroll
+        for (int m = N - 1; m >= 1; --m) {
+            // Horner down to level max(m, Q) inside the slice
+            const int stop = m > Q ? m : Q;
+            Real g0[GMAX], g1[GMAX];
+#pragma unroll
+            for (int J = 0; J < GMAX; ++J) g0[J] = cb[LY::top_off(N) + J];
+#pragma unroll
+            for (int l = N - 1; l >= Q; --l) {
+                if (l >= stop) {
+                    const Real inv = Real(1) / Real(l - m + 1);
+#pragma unroll
+                    for (int J = 0; J < ipow(d, l - Q); ++J) {
+                        Real acc = Real(0);
+#pragma unroll
+                        for (int c = 0; c < d; ++c) acc += ((N - 1 - l) % 2 == 0 ? g0[J * d + c] : g1[J * d + c]) * dl[c];
+                        const Real v = cb[LY::top_off(l) + J] + inv * acc;
+                        if ((N - 1 - l) % 2 == 0) g1[J] = v;
+                        else g0[J] = v;
+                    }
+                }
+            }
+            const bool in1 = (N - 1 - stop) % 2 == 0;  // the last stage wrote g1
+            if (m >= Q) {
+#pragma unroll
+                for (int J = 0; J < ipow(d, m - Q > 0 ? m - Q : 0); ++J) ab[LY::top_off(m) + J] = in1 ? g1[J] : g0[J];
+            } else {
+                gq[m] = in1 ? g1[0] : g0[0];
+            }
+        }
+        // targets m < Q: continue across lanes, level l = Q-1 .. m (segmented sums over digit l+1)
+#pragma unroll
+        for (int m = Q - 1; m >= 1; --m) {
+            Real gcur = gq[m];
+#pragma unroll
+            for (int l = Q - 1; l >= 1; --l) {
+                if (l >= m) {
+                    __syncwarp();
+                    rd[lane][0] = gcur * dp[l + 1];
+                    __syncwarp();
+                    // idle lanes (lane >= SLOTS*P) read their own slot's range clamped to slot 0
+                    const int stride = ipow(d, Q - l - 1);
+                    const int base = (lane_on ? slot : 0) * P + (p / ipow(d, Q - l)) * ipow(d, Q - l);
+                    Real sum = Real(0);
+#pragma unroll
+                    for (int c = 0; c < d; ++c) sum += rd[base + c * stride][0];
+                    gcur = sc(cb, l) + (Real(1) / Real(l - m + 1)) * sum;
+                }
+            }
+            ab[m - 1] = gcur;
+        }
+        // ---- δ̄_s = segmented sum of the lanes' partials
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < d; ++c) {
+            Real v = gd[c];
+#pragma unroll
+            for (int k = 1; k <= Q; ++k) v += dg[k] == c ? gk[k] : Real(0);
+            rd[lane][c] = v;
+        }
+        __syncwarp();
+        if (on && p < d) {
+            Real sum = Real(0);
+            for (int q = 0; q < P; ++q) sum += rd[slot * P + q][p];
+            dbar[(b * M + s) * d + p] = sum;
+        }
+#pragma unroll
+        for (int i = 0; i < S; ++i) cb[i] = on ? ab[i] : cb[i];
+    }
+}
+
+}  // namespace sigk
