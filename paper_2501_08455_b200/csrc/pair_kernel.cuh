@@ -383,7 +383,7 @@ __device__ __forceinline__ void fused_scan(const CombineSmem<d, N, P1S>& S, int 
             for (int a = A0; a <= E; ++a) {
                 idx[a] = I / ipow(d, E - a);
                 wr[a] = I % ipow(d, E - a) == 0;
-                P[a] = (a == 1) ? S.p10[idx[1]] : (S.p0 ? S.p0[level_off(d, a - 1) + idx[a]] : 0.f);
+                P[a] = (a == 1) ? S.p10[idx[1]] : (S.p0 ? __ldcg(S.p0 + level_off(d, a - 1) + idx[a]) : 0.f);  // p0: a previous launch's output, via L2
                 if (wr[a]) S.pf[level_off(d, a - 1) + idx[a]] = P[a];
             }
 #pragma unroll 4
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(256) segment_prefix_kernel(const float* __rest
     pdl_wait();  // the segment rows come from the previous launch
     for (int i = tid; i < G * D; i += nth) {
         const int j = i / D, r = i - (i / D) * D;
-        const float v = Rb[i];
+        const float v = __ldcg(Rb + i);  // written by the previous launch: via L2
         if (r < DL) S.ylow[(size_t)j * DL + r] = v;
         else top[(size_t)j * LN + r - DL] = v;
     }

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
     }
     __syncthreads();
     for (int F = tid; F < LN; F += nth) {  // exclusive scan over chunks, fixed order
-        float run = pre0 != nullptr ? pre0[DL + F] : 0.f;  // P^(0)_N
+        float run = pre0 != nullptr ? __ldcg(pre0 + DL + F) : 0.f;  // P^(0)_N (a previous launch's output: via L2)
         top[F] = run;
         for (int j = 1; j <= U; ++j) {
             run += top[(size_t)j * LNP + F];

@@ -171,6 +171,20 @@ struct SliceRev {
 };
 
 template <typename Real, int d, int N, int Q>
+struct SliceGather {
+    using LY = SliceLayout<d, N, Q>;
+    template <int n>
+    __device__ __forceinline__ static void level(const Real* __restrict__ row, bool ok, const int (&lvl)[N - Q + 1],
+                                                 Real (&dst)[LY::S]) {
+        if constexpr (n <= N) {
+#pragma unroll
+            for (int r = 0; r < ipow(d, n - Q); ++r) dst[LY::top_off(n) + r] = ok ? __ldcg(row + lvl[n - Q] + r) : Real(0);
+            level<n + 1>(row, ok, lvl, dst);
+        }
+    }
+};
+
+template <typename Real, int d, int N, int Q>
 __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__ X, int64_t L, int64_t items,
                                                         int U, int64_t CL, const Real* __restrict__ states,
                                                         const Real* __restrict__ cbars, Real* __restrict__ dbar) {
@@ -192,29 +206,30 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
     for (int k = 1; k <= Q; ++k) dg[k] = (p / ipow(d, Q - k)) % d;
     Real (&rd)[32][d + 1] = red[warp];
 
-    // element offsets of the lane's slice inside a signature row
-    auto row_off = [&](int i) -> int {
-        // i < NLOW: level i+1 scalar at prefix p_1..p_{i+1}; else level n slice entry
-        if (i < NLOW) return level_off(d, i) + p / ipow(d, Q - (i + 1));
-        int n = Q, o = NLOW;
-        while (i >= o + ipow(d, n - Q)) {
-            o += ipow(d, n - Q);
-            ++n;
-        }
-        return level_off(d, n - 1) + p * ipow(d, n - Q) + (i - o);
-    };
+    // the lane's slice inside a signature row: low scalars at level k (k < Q),
+    // then level n >= Q at lvl[n - Q] .. + d^(n-Q) (per-lane bases, compile-time layout)
+    int low[Q], lvl[N - Q + 1];
+#pragma unroll
+    for (int k = 1; k < Q; ++k) low[k - 1] = level_off(d, k - 1) + p / ipow(d, Q - k);
+#pragma unroll
+    for (int n = Q; n <= N; ++n) lvl[n - Q] = level_off(d, n - 1) + p * ipow(d, n - Q);
     Real cb[S], a[S], an[S];
     const Real* crow = cbars + it * D;
+    auto gather = [&](const Real* __restrict__ row, bool ok, Real(&dst)[S]) {
+#pragma unroll
+        for (int k = 1; k < Q; ++k) dst[k - 1] = ok ? __ldcg(row + low[k - 1]) : Real(0);
+        SliceGather<Real, d, N, Q>::template level<Q>(row, ok, lvl, dst);
+    };
     const Real* xb = X + b * L * d;
     const Real* sb = states + b * M * D;
     auto load_state = [&](int64_t s, Real (&dst)[S]) {  // S_s = row s-1; identity (zeros) for s <= 0
-#pragma unroll
-        for (int i = 0; i < S; ++i) dst[i] = (valid && s >= 1 && s <= M) ? __ldg(sb + (s - 1) * D + row_off(i)) : Real(0);
+        const bool ok = valid && s >= 1 && s <= M;
+        gather(sb + (ok ? s - 1 : 0) * D, ok, dst);
     };
     pdl_trigger();
-    pdl_wait();  // cbars and states come from the previous launches
-#pragma unroll
-    for (int i = 0; i < S; ++i) cb[i] = valid ? crow[row_off(i)] : Real(0);
+    pdl_wait();  // cbars and states come from the previous launches: read them through L2
+                 // (ld.global.cg), never through an L1 line filled while those launches ran
+    gather(crow, valid, cb);
     // scal(k): A_k / C̄_k at prefix p_1..p_k for k <= Q
     auto sc = [&](Real (&v)[S], int k) -> Real& { return k < Q ? v[k - 1] : v[NLOW]; };
     load_state(s_hi - 1, an);
