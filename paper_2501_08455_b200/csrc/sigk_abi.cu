@@ -1020,7 +1020,8 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     // kernels on the gathered chunks) give the cotangent at every chunk end
     const int sms = device_info([] { int v = 0; cudaGetDevice(&v); return v; }()).sms;
     int U = 1;
-    if (M >= 32 && (tun == nullptr || tun->chunks != 1)) {
+    // (the boundary pass stages 3 rows of D in shared memory; wider signatures walk whole paths)
+    if (M >= 32 && (tun == nullptr || tun->chunks != 1) && 3 * sizeof(Real) * (size_t)D <= 227 * 1024) {
         const int64_t want = ((int64_t)sms * 8 + B - 1) / B;
         U = (int)std::max<int64_t>(1, std::min<int64_t>(want, M / 16));
         if (tun && tun->chunks > 1) U = (int)std::min<int64_t>(tun->chunks, M);
@@ -1045,7 +1046,10 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             release();
             return rc;
         }
-        vjp_boundary_kernel<Real><<<(unsigned)B, 256, 0, s>>>(C, cot, cb, U, d, N, D);
+        const size_t bsm = 3 * sizeof(Real) * (size_t)D;
+        if (bsm > 48 * 1024)
+            cudaFuncSetAttribute(vjp_boundary_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
+        vjp_boundary_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, cot, cb, U, d, N, D);
         cbars = cb;
         launches += 2 + cst.launches;
     }

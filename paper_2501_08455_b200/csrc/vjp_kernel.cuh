@@ -257,6 +257,13 @@ __global__ void segment_gather_kernel(const Real* __restrict__ X, int64_t B, int
 template <typename Real>
 __global__ void __launch_bounds__(256) vjp_boundary_kernel(const Real* __restrict__ C, const Real* __restrict__ cot,
                                                            Real* __restrict__ cbars, int U, int d, int N, int64_t D) {
+    // dynamic shared memory: the running cotangent row and the chunk signature
+    // row (2 D values), staged once per chunk so the contractions read shared
+    // memory rather than chains of dependent global loads
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* cur = reinterpret_cast<Real*>(smem_raw);
+    Real* sig = cur + D;
+    Real* nxt = sig + D;
     __shared__ int64_t off[kGenericMaxDepth + 1];
     const int64_t b = blockIdx.x;
     const int tid = threadIdx.x, nth = blockDim.x;
@@ -271,25 +278,33 @@ __global__ void __launch_bounds__(256) vjp_boundary_kernel(const Real* __restric
     pdl_trigger();
     pdl_wait();
     Real* cb = cbars + b * U * D;
-    for (int64_t i = tid; i < D; i += nth) cb[(int64_t)(U - 1) * D + i] = cot[b * D + i];
-    __syncthreads();
+    for (int64_t i = tid; i < D; i += nth) {
+        const Real v = __ldcg(cot + b * D + i);
+        cur[i] = v;
+        cb[(int64_t)(U - 1) * D + i] = v;
+    }
     for (int j = U - 1; j >= 1; --j) {
-        const Real* src = cb + (int64_t)j * D;
         const Real* cj = C + (b * U + j) * D;
-        Real* dst = cb + (int64_t)(j - 1) * D;
+        for (int64_t i = tid; i < D; i += nth) sig[i] = __ldcg(cj + i);  // a previous launch's output: via L2
+        __syncthreads();
         for (int n = 1; n <= N; ++n) {
             const int64_t sz = off[n] - off[n - 1];
             for (int64_t I = tid; I < sz; I += nth) {
-                Real acc = src[off[n - 1] + I];
+                Real acc = cur[off[n - 1] + I];
                 int64_t w = 1;
                 for (int k = 1; n + k <= N; ++k) {
                     w *= d;
-                    const Real* cr = src + off[n + k - 1] + I * w;
-                    const Real* er = cj + off[k - 1];
+                    const Real* cr = cur + off[n + k - 1] + I * w;
+                    const Real* er = sig + off[k - 1];
                     for (int64_t J = 0; J < w; ++J) acc = fma(cr[J], er[J], acc);
                 }
-                dst[off[n - 1] + I] = acc;
+                nxt[off[n - 1] + I] = acc;
             }
+        }
+        __syncthreads();
+        for (int64_t i = tid; i < D; i += nth) {
+            cur[i] = nxt[i];
+            cb[(int64_t)(j - 1) * D + i] = nxt[i];
         }
         __syncthreads();
     }
