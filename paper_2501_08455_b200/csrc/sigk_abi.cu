@@ -1087,7 +1087,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = getenv("SIGK_VJP_NOPDL") ? 0 : 1;
+        cfg.numAttrs = 1;
         e = cudaLaunchKernelEx(&cfg, sl.fn, X, L, items, U, CL, static_cast<const Real*>(states), cbars, dbar);
         if (e != cudaSuccess) {
             release();
