@@ -41,6 +41,7 @@ def _units():
     units.append(("sigkit_api", os.path.join(CSRC, "sigkit_api.cpp"), []))
     units.append(("bench_api", os.path.join(CSRC, "bench_api.cpp"), []))
     units.append(("model_api", os.path.join(CSRC, "model_api.cpp"), []))
+    units.append(("model_gpu", os.path.join(CSRC, "model_gpu.cu"), []))
     return units
 
 
