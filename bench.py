@@ -480,9 +480,11 @@ def run_reference(args):
     X = np.zeros((B, L, d), np.float64)
     X[:, 1:] = np.cumsum(rng.standard_normal((B, L - 1, d)) / math.sqrt(L - 1), axis=1)
     X = X.astype(np.float32).astype(np.float64)  # same fp32-representable inputs as the GPU arm
-    # bounded sample per step: enough rows for ~1 s of work on all threads
-    t1, kind = cpu_reference_run(X[:threads], N, threads)
-    rows = int(max(1, min(B, threads * max(1.0, 1.0 / max(t1, 1e-6)))))
+    # bounded sample per step: whole waves of `threads` rows, <= ~1 s per step and
+    # <= ~90 s for the whole --steps/--warmup run
+    t1, kind = cpu_reference_run(X[:threads], N, threads)  # one wave: `threads` rows in parallel
+    target = min(1.0, 90.0 / max(1, args.steps + args.warmup))
+    rows = int(max(1, min(B, threads * max(1, int(target / max(t1, 1e-6))))))
     Xs = X[:rows]
     for _ in range(args.warmup):
         cpu_reference_run(Xs, N, threads)
@@ -526,7 +528,7 @@ def main():
     TUNE.update(chunks=args.chunks, prefix_len=args.prefix_len, segments=args.segments, family=fam)
     if args.impl == "reference":
         args.steps = args.steps or 5
-        args.warmup = 1 if args.warmup is None else args.warmup
+        args.warmup = max(3, 3 if args.warmup is None else args.warmup)
         run_reference(args)
         return
     default_steps = {"c1": 20000, "c2": 20000, "c3": 2000, "c4": 500, "c5": 100}[args.config]
