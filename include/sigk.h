@@ -162,6 +162,15 @@ int sigk_brownian_f64(double* X_dev, size_t B, size_t L, int d, uint64_t seed, s
  * random walks from (seed, B, L, d), bit-identical to make_bench_paths. */
 int sigk_make_bench_paths(uint64_t seed, size_t B, size_t L, int d, double* out);
 
+/* Brute-force signature of ONE host path (len points, dim channels) by
+ * direct enumeration of segment-index tuples (reference
+ * signature_bruteforce, oracle.hpp:23-31, oracle.cpp:28-96; strict = 1 for
+ * TupleClass::StrictlyIncreasing). One GPU thread per coefficient, the
+ * reference's enumeration order and products: fp64 bit-identical. Limits as
+ * the reference's OracleLimits: SIGK_ERESOURCE beyond them. Synchronous. */
+int sigk_signature_bruteforce_f64(const double* path, size_t len, int dim, int depth, int max_segments,
+                                  int max_depth, int max_dim, int strict, double* out);
+
 /* Increments X[:, k+1] - X[:, k] into out (B, L-1, d) (reference
  * increments, kernels.cpp:71-87), and increments divided by m! for m =
  * 2..depth into out (depth-1, n) (reference scaled_increments,

@@ -96,6 +96,7 @@ def ref():
             lib.ref_finite_diff_grad.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp, C.c_double, _dp]
             lib.ref_increments.argtypes = [_dp, _sz, _sz, C.c_int, _dp]
             lib.ref_scaled_increments.argtypes = [_dp, _sz, _sz, C.c_int, C.c_int, _dp]
+            lib.ref_bruteforce_strict.argtypes = [_dp, _sz, C.c_int, C.c_int, _dp]
             lib.ref_train.argtypes = [_sz, _sz, C.c_int, C.c_int, _sz, C.c_int, C.c_double, C.c_uint64, C.c_int,
                                       C.c_int, _dp]
             _ref = lib
@@ -196,6 +197,15 @@ def ref_stream(X: np.ndarray, N: int) -> np.ndarray:
     B, L, d = X.shape
     out = np.empty((B, L - 1, sig_dim(d, N)), np.float64)
     _ref_call(ref().ref_signature_stream(_ptr(X, _dp), B, L, d, N, _ptr(out, _dp)))
+    return out
+
+
+def ref_bruteforce_strict(path: np.ndarray, N: int) -> np.ndarray:
+    """The reference's signature_bruteforce with TupleClass::StrictlyIncreasing."""
+    path = np.ascontiguousarray(path, np.float64)
+    L, d = path.shape
+    out = np.empty(sig_dim(d, N))
+    _ref_call(ref().ref_bruteforce_strict(_ptr(path, _dp), L, d, N, _ptr(out, _dp)))
     return out
 
 

@@ -145,6 +145,15 @@ int ref_bruteforce(const double* path, std::size_t L, int d, int N, double* out)
     });
 }
 
+// signature_bruteforce with the strict tuple class (oracle.cpp:28-96)
+int ref_bruteforce_strict(const double* path, std::size_t L, int d, int N, double* out) {
+    return guarded([&] {
+        std::vector<double> p(path, path + L * static_cast<std::size_t>(d));
+        auto f = sigkit::signature_bruteforce(p, L, d, N, sigkit::OracleLimits{}, sigkit::TupleClass::StrictlyIncreasing);
+        std::memcpy(out, f.coeffs.data(), f.coeffs.size() * sizeof(double));
+    });
+}
+
 // flatten(chen_product(unflatten(a), unflatten(b))) (tensor_algebra.cpp:80-127).
 int ref_chen_product(int d, int N, const double* a, const double* b, double* c) {
     return guarded([&] {

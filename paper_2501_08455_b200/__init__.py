@@ -149,6 +149,7 @@ def lib():
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, vp, C.c_uint, vp]
         for n in ("sigk_scaled_increments_f32", "sigk_scaled_increments_f64"):
             getattr(L, n).argtypes = [vp, sz, C.c_int, vp, C.c_uint, vp]
+        L.sigk_signature_bruteforce_f64.argtypes = [vp, sz, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp]
         L.sigk_train.argtypes = [sz, sz, C.c_int, C.c_int, sz, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int,
                                  C.POINTER(C.c_double)]
         L.sigk_last_error.restype = C.c_char_p
@@ -441,6 +442,20 @@ def increments(paths):
     return out
 
 
+def signature_bruteforce(path, depth: int, max_segments: int = 8, max_depth: int = 4, max_dim: int = 3,
+                         strict: bool = False) -> np.ndarray:
+    """Reference ``signature_bruteforce`` (oracle.cpp:28-96): one (L, d) path by tuple enumeration, on the GPU
+    (fp64, bit-identical). Limits as the reference's OracleLimits (ResourceError beyond them)."""
+    p = np.ascontiguousarray(path, np.float64)
+    if p.ndim != 2:
+        raise DomainError("signature_bruteforce: path must have shape (L, d)")
+    L, d = p.shape
+    out = np.empty(sig_dim(d, depth) if d >= 1 and depth >= 1 else 0)
+    _check(lib().sigk_signature_bruteforce_f64(p.ctypes.data if p.size else None, L, d, depth, max_segments,
+                                               max_depth, max_dim, int(strict), out.ctypes.data if out.size else None))
+    return out
+
+
 def scaled_increments(inc, depth: int) -> list:
     """Reference ``scaled_increments`` (kernels.cpp:89-104): [inc / m! for m = 2..depth] on the GPU."""
     a = np.ascontiguousarray(inc if np.asarray(inc).dtype in (np.float32, np.float64) else np.asarray(inc, np.float64))
@@ -483,7 +498,7 @@ __all__ = [
     "DomainError", "ResourceError", "TrainingError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
-    "signature_stream", "signature_vjp", "TrainConfig", "train", "increments", "scaled_increments",
+    "signature_stream", "signature_vjp", "TrainConfig", "train", "increments", "scaled_increments", "signature_bruteforce",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
     "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES", "SIGK_X_ON_DEVICE", "SIGK_OUT_ON_DEVICE", "SIGK_ASYNC_HOST",
 ]

@@ -19,6 +19,7 @@
 #include "variants.h"
 #include "vjp_kernel.cuh"
 #include "increments.cuh"
+#include "bruteforce.cuh"
 
 namespace sigk {
 
@@ -1275,6 +1276,34 @@ int sigk_signature_f32(const float* X, size_t B, size_t L, int d, int N, float* 
 int sigk_signature_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags, void* stream,
                        const sigk_tuning* tuning, sigk_stats* stats) {
     return sigk::signature_impl<double>(X, B, L, d, N, out, flags, stream, tuning, stats);
+}
+
+int sigk_signature_bruteforce_f64(const double* path, size_t len, int dim, int depth, int max_segments,
+                                  int max_depth, int max_dim, int strict, double* out) {
+    sigk::g_err.clear();
+    if (len < 1 || dim < 1 || depth < 1)
+        return sigk::fail(SIGK_EDOMAIN, "signature_bruteforce: len, dim and depth must be >= 1");
+    if (path == nullptr || out == nullptr) return sigk::fail(SIGK_EDOMAIN, "signature_bruteforce: null pointer");
+    const int segments = (int)len - 1;
+    if (segments > max_segments || depth > max_depth || dim > max_dim || depth > sigk::kBruteMaxDepth)
+        return sigk::fail(SIGK_ERESOURCE, "signature_bruteforce: instance exceeds limits (segments " +
+                                              std::to_string(segments) + "/" + std::to_string(max_segments) +
+                                              ", depth " + std::to_string(depth) + "/" + std::to_string(max_depth) +
+                                              ", dim " + std::to_string(dim) + "/" + std::to_string(max_dim) + ")");
+    size_t D = 0;
+    sigk_sig_dim(dim, depth, &D);
+    double *dp = nullptr, *dq = nullptr;
+    cudaError_t e = cudaMalloc(&dp, sizeof(double) * len * dim);
+    if (e == cudaSuccess) e = cudaMalloc(&dq, sizeof(double) * D);
+    if (e == cudaSuccess) e = cudaMemcpy(dp, path, sizeof(double) * len * dim, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        sigk::bruteforce_kernel<<<(unsigned)((D + 127) / 128), 128>>>(dp, segments, dim, depth, strict, dq);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, dq, sizeof(double) * D, cudaMemcpyDeviceToHost);
+    cudaFree(dp);
+    cudaFree(dq);
+    return e == cudaSuccess ? SIGK_OK : sigk::cuda_fail(e, "signature_bruteforce");
 }
 
 int sigk_increments_f32(const float* X, size_t B, size_t L, int d, float* out, unsigned flags, void* stream) {

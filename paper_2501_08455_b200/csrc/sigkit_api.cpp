@@ -9,6 +9,7 @@
 #include "sigk.h"
 #include "sigkit/autodiff.hpp"
 #include "sigkit/kernels.hpp"
+#include "sigkit/oracle.hpp"
 #include "sigkit/tensor_algebra.hpp"
 
 namespace sigkit {
@@ -184,6 +185,22 @@ ExecutionCaps ExecutionCaps::detect() {
 KernelKind select_kernel(KernelKind hint, const ExecutionCaps& caps, std::size_t seq_len) {
     if (hint != KernelKind::Auto) return hint;
     return (caps.accelerated && seq_len >= caps.parallel_min_len) ? KernelKind::Parallel : KernelKind::Sequential;
+}
+
+FlatSignature signature_bruteforce(const std::vector<double>& path, std::size_t len, int dim, int depth,
+                                   const OracleLimits& limits, TupleClass tuples) {
+    if (len < 1 || dim < 1 || depth < 1) throw DomainError("signature_bruteforce: len, dim and depth must be >= 1");
+    if (path.size() != len * static_cast<std::size_t>(dim))
+        throw DomainError("signature_bruteforce: path size does not match (len, dim)");
+    FlatSignature out;
+    out.dim = dim;
+    out.depth = depth;
+    out.coeffs.assign(sig_dim(dim, depth), 0.0);
+    const int rc = sigk_signature_bruteforce_f64(path.data(), len, dim, depth, limits.max_segments, limits.max_depth,
+                                                 limits.max_dim, tuples == TupleClass::StrictlyIncreasing ? 1 : 0,
+                                                 out.coeffs.data());
+    if (rc != SIGK_OK) rethrow(rc);
+    return out;
 }
 
 IncrementBatch increments(const PathBatch& paths) {

@@ -11,6 +11,7 @@
 
 #include "sigkit/errors.hpp"
 #include "sigkit/kernels.hpp"
+#include "sigkit/oracle.hpp"
 #include "sigkit/tensor_algebra.hpp"
 
 using namespace sigkit;
@@ -159,6 +160,19 @@ int main() {
         PathBatch one = random_paths(78, 2, 1, 3, 1.0);
         CHECK(increments(one).diffs.empty());
         CHECK(scaled_increments(increments(p), 1).per_degree.empty());
+    }
+
+    // signature_bruteforce (oracle.hpp; test_oracle.cpp:27-45): corner path and limits
+    {
+        const std::vector<double> corner = {0, 0, 1, 0, 1, 1};
+        const FlatSignature f = signature_bruteforce(corner, 3, 2, 2);
+        const double want[6] = {1, 1, 0.5, 1, 0, 0.5};
+        bool ok = f.coeffs.size() == 6;
+        for (int i = 0; ok && i < 6; ++i) ok = std::abs(f.coeffs[i] - want[i]) <= 1e-12;
+        CHECK(ok);
+        bool threw = false;
+        try { signature_bruteforce(std::vector<double>(20, 0.0), 10, 2, 2); } catch (const ResourceError&) { threw = true; }
+        CHECK(threw);
     }
 
     std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);

@@ -56,3 +56,22 @@ def test_increments_errors(sk):
         sk.increments(np.zeros((0, 3, 2)))
     with pytest.raises(sk.DomainError):
         sk.scaled_increments(np.zeros((1, 2, 2)), 0)
+
+
+@pytest.mark.parametrize("L,d,N", [(1, 2, 2), (2, 3, 4), (5, 2, 3), (9, 3, 4), (9, 1, 4), (4, 3, 1)])
+def test_bruteforce_matches_reference(sk, L, d, N):
+    # reference signature_bruteforce (oracle.cpp:28-96), both tuple classes, fp64 bit-identical
+    path = np.random.default_rng(L * 10 + d).standard_normal((L, d))
+    assert np.array_equal(sk.signature_bruteforce(path, N), O.ref_bruteforce(path, N))
+    assert np.array_equal(sk.signature_bruteforce(path, N, strict=True), O.ref_bruteforce_strict(path, N))
+
+
+def test_bruteforce_limits(sk):
+    with pytest.raises(sk.ResourceError):
+        sk.signature_bruteforce(np.zeros((10, 2)), 3)  # 9 segments > 8
+    with pytest.raises(sk.ResourceError):
+        sk.signature_bruteforce(np.zeros((3, 4)), 2)  # dim 4 > 3
+    with pytest.raises(sk.DomainError):
+        sk.signature_bruteforce(np.zeros((3, 2)), 0)
+    big = sk.signature_bruteforce(np.random.default_rng(0).standard_normal((12, 2)), 5, max_segments=11, max_depth=5)
+    assert big.shape == (62,)
