@@ -550,55 +550,6 @@ __device__ __forceinline__ void segment_combine_path(const float* __restrict__ R
     }
 }
 
-// Exclusive prefix products of the G segment rows of every path (one CTA
-// per path): prefix row g = signature of X[0 .. start of segment g] (row 0 the
-// identity: zeros), with the combine formulas of segment_combine_path; the
-// prefix-stream kernel starts segment g from it.
-template <int d, int N, bool P1S>
-__global__ void __launch_bounds__(256) segment_prefix_kernel(const float* __restrict__ rows, int G,
-                                                             float* __restrict__ prefix) {
-    using CLY = CombineLayout<d, N>;
-    constexpr int D = level_off(d, N), DL = CLY::DL, LN = CLY::LN;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* smem = reinterpret_cast<float*>(smem_raw);
-    const int64_t b = blockIdx.x;
-    const float* Rb = rows + b * G * D;
-    float* pb = prefix + b * G * D;
-    CombineSmem<d, N, P1S> S(smem, G);
-    float* top = smem + CLY::floats(G, 0);  // [G][LN]
-    const int tid = threadIdx.x, nth = blockDim.x;
-    pdl_trigger();
-    pdl_wait();  // the segment rows come from the previous launch
-    for (int i = tid; i < G * D; i += nth) {
-        const int j = i / D, r = i - (i / D) * D;
-        const float v = __ldcg(Rb + i);  // written by the previous launch: via L2
-        if (r < DL) S.ylow[(size_t)j * DL + r] = v;
-        else top[(size_t)j * LN + r - DL] = v;
-    }
-    if (tid < d) S.p10[tid] = 0.f;
-    __syncthreads();
-    fused_scan<d, N, P1S>(S, G, tid, nth);
-    build_c<d, N, P1S>(S, G, tid, nth);
-    __syncthreads();
-    for (int i = tid; i < G * DL; i += nth) pb[(size_t)(i / DL) * D + i % DL] = S.pf[i];  // P^(g), levels < N
-    for (int F = tid; F < LN; F += nth) {
-        float acc = 0.f;
-        for (int j = 0; j < G; ++j) {
-            pb[(size_t)j * D + DL + F] = acc;  // exclusive: level N of P^(j)
-            float x = top[(size_t)j * LN + F];
-            if constexpr (N == 1 && P1S) {
-                if (j != G - 1) x = 0.f;
-            }
-#pragma unroll
-            for (int a = (P1S ? 2 : 1); a < N; ++a) {
-                const int tail = ipow(d, N - a);
-                x = fmaf(S.pf[(size_t)j * DL + level_off(d, a - 1) + F / tail], S.crow(j, N - a)[F % tail], x);
-            }
-            acc += x;
-        }
-    }
-}
-
 // Steps 1-2 of a pair-family CTA (also used by the prefix-stream kernel):
 // stage the segment's points X[seg0 .. seg0+slen] into `raw` and build the
 // δ table `tab` ([CL][UP][RS] pairs). Returns the (shifted) raw pointer. The
@@ -707,7 +658,12 @@ struct PairGeom {
     int* counters;      // G > 1: [B] arrival counters (zero between launches)
     int smem_bytes;     // dynamic shared memory of the launch (the last 16 bytes hold a flag)
     float* final_out;   // G > 1: (B, D) signatures (the kernel's `out` then holds the (B*G, D) segment rows)
-    const float* prefix = nullptr;  // prefix-stream kernel, G > 1: (B*G, D) signature of X[0 .. segment start]
+    // prefix-stream kernel, G > 1, in-kernel look-back: CTA (b, g) publishes the
+    // signature of X[0 .. end of its segment] in pub row b*G + g and sets
+    // flags[b*G + g] = epoch (a per-call value, so flags never need resetting)
+    float* pub = nullptr;
+    int* flags = nullptr;
+    int epoch = 0;
 };
 
 template <int d, int N, int Q>

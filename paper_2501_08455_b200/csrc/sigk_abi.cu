@@ -340,7 +340,7 @@ static void* segment_scratch(int dev, cudaStream_t s, int kind, size_t bytes, bo
     if (capturing) {
         void* p = nullptr;
         if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
-        if (kind == 1 && cudaMemsetAsync(p, 0, bytes, s) != cudaSuccess) return nullptr;
+        if ((kind == 1 || kind == 12) && cudaMemsetAsync(p, 0, bytes, s) != cudaSuccess) return nullptr;
         *async_alloc = true;
         return p;
     }
@@ -353,7 +353,7 @@ static void* segment_scratch(int dev, cudaStream_t s, int kind, size_t bytes, bo
     }
     void* p = nullptr;
     if (cudaMalloc(&p, n) != cudaSuccess) return nullptr;
-    if (kind == 1 && cudaMemset(p, 0, n) != cudaSuccess) return nullptr;
+    if ((kind == 1 || kind == 12) && cudaMemset(p, 0, n) != cudaSuccess) return nullptr;  // counters, flags
     if (hit) {
         hit->p = p;
         hit->n = n;
@@ -814,6 +814,18 @@ static int scaled_increments_impl(const Real* inc, size_t n, int depth, Real* ou
 // (B, L-1, D), row t = signature of X[0..t+1]. fp32 shapes with a pair
 // variant use the two-pass chunk-pair stream kernel (stream_kernel.cuh); the
 // rest use the element-parallel generic stream kernel.
+// Per-(device, stream) launch epochs of the look-back stream kernel (flags
+// hold the epoch of the launch that set them, so they are never reset).
+static int next_stream_epoch(int dev, cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, cudaStream_t>, int>> tab;
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& kv : tab)
+        if (kv.first.first == dev && kv.first.second == s) return kv.second = kv.second % 0x7ffffffe + 1;
+    tab.emplace_back(std::make_pair(dev, s), 1);
+    return 1;
+}
+
 template <typename Real>
 static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* out, cudaStream_t s,
                          const sigk_tuning* tun, sigk_stats* st) {
@@ -844,45 +856,32 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
             // (C2: U 10 -> 20, 102 -> 88 µs)
             const int sms = device_info(dev).sms;
             // segments per path: one CTA per path leaves SMs idle for small
-            // batches, so split each path into G pieces started from their
-            // true prefixes (the pair kernel's segment rows, scanned by
-            // segment_prefix_kernel); >= 64 steps per piece
+            // batches, so split each path into G pieces whose CTAs chain their
+            // prefixes in-kernel; >= 64 steps per piece
             int G = tun && tun->segments > 0 ? tun->segments : 1;
             if (!(tun && tun->segments > 0)) {
-                G = (int)std::max<int64_t>(1, std::min<int64_t>(8, sms / B));  // measured: B*G ~ SMs
+                G = (int)std::max<int64_t>(1, std::min<int64_t>(4, sms / B));  // measured: B*G ~ SMs, <= 4
                 while (G > 1 && M / G < 64) --G;
             }
             G = (int)std::max<int64_t>(1, std::min<int64_t>(G, M));
             int64_t SL = (M + G - 1) / G;
-            const void* prefix = nullptr;
+            // G > 1: the segment CTAs of a path chain their prefixes in-kernel
+            // (decoupled look-back: CTA g waits for the row CTA g-1 publishes)
+            void* pub = nullptr;
+            int* flags = nullptr;
+            int epoch = 0;
             if (G > 1) {
-                sigk_tuning ts = tp;
-                ts.segments = G;
-                ts.chunks = 0;
-                const Plan sp = cached_plan(d, N, false, dev, B, M, D, &ts);
-                if (!sp.v || !sp.v->prefix_launch || sp.G != G) {
-                    G = 1;
+                cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+                cudaStreamIsCapturing(s, &cap);
+                if (cap != cudaStreamCaptureStatusNone) {
+                    G = 1;  // look-back epochs are host-side state: not capturable
                     SL = M;
                 } else {
-                    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-                    cudaStreamIsCapturing(s, &cap);
-                    const bool capt = cap != cudaStreamCaptureStatusNone;
-                    bool a1 = false, a2 = false, a3 = false, a4 = false;
-                    void* rows = segment_scratch(dev, s, 8, sizeof(float) * B * G * D, capt, &a1);
-                    void* ctr = segment_scratch(dev, s, 1, sizeof(int) * B, capt, &a2);
-                    void* fin = segment_scratch(dev, s, 9, sizeof(float) * B * D, capt, &a3);
-                    void* pre = segment_scratch(dev, s, 10, sizeof(float) * B * G * D, capt, &a4);
-                    if (!rows || !ctr || !fin || !pre) return fail(SIGK_ERESOURCE, "stream segment scratch");
-                    const int CL2 = (int)((SL + sp.U - 1) / sp.U);
-                    PairLaunch a{X, B, L, G, SL, sp.U, CL2, fin, rows, ctr, s, false, nullptr, nullptr, capt, nullptr};
-                    e = sp.v->pair_launch(a);
-                    if (e == cudaSuccess) e = sp.v->prefix_launch(rows, B, G, pre, s);
-                    for (auto q : {std::make_pair(a1, rows), std::make_pair(a3, fin), std::make_pair(a4, pre)})
-                        if (q.first) cudaFreeAsync(q.second, s);
-                    if (a2) cudaFreeAsync(ctr, s);
-                    if (e != cudaSuccess) return cuda_fail(e, "stream segment prefixes");
-                    prefix = pre;
-                    local.launches += 2;
+                    bool a1 = false, a2 = false;
+                    pub = segment_scratch(dev, s, 11, sizeof(float) * B * G * D, false, &a1);
+                    flags = static_cast<int*>(segment_scratch(dev, s, 12, sizeof(int) * B * G, false, &a2));
+                    if (!pub || !flags) return fail(SIGK_ERESOURCE, "stream segment scratch");
+                    epoch = next_stream_epoch(dev, s);
                     local.segments = G;
                 }
             }
@@ -890,7 +889,7 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
             if (!(tun && tun->chunks > 0) && B * G <= sms)
                 U = std::max(U, (int)std::min<int64_t>(2 * plan.v->pair_units_max, std::max<int64_t>(2, SL / 8)));
             for (;;) {
-                e = plan.v->stream_launch(X, B, L, U, out, s, overlap || G > 1, G, prefix);
+                e = plan.v->stream_launch(X, B, L, U, out, s, overlap, G, pub, flags, epoch);
                 if (e != cudaErrorInvalidValue || U <= plan.U) break;
                 cudaGetLastError();
                 U = std::max(plan.U, U - 2);

@@ -100,13 +100,15 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
     constexpr int DL = CLY::DL, LN = CLY::LN, LNP = CLY::LNP, FJ = PF::FJ;
     extern __shared__ __align__(16) unsigned char smem_raw[];
 
-    // CTA (b, sg): steps [sg*SL, (sg+1)*SL) of path b, started from g.prefix row
-    // (b*G + sg) when the path is split (G > 1)
+    // CTA (b, sg): steps [sg*SL, (sg+1)*SL) of path b (G > 1: the path is split)
     const int64_t b = blockIdx.x / g.G, sg = blockIdx.x - (blockIdx.x / g.G) * g.G;
     const int64_t M = L - 1;
     const int64_t seg0 = sg * g.SL < M ? sg * g.SL : M;
     const int64_t slen = (seg0 + g.SL < M ? seg0 + g.SL : M) - seg0;
-    const float* __restrict__ pre0 = g.prefix != nullptr ? g.prefix + (b * g.G + sg) * D : nullptr;
+    // P^(0) of the segment: the inclusive prefix published by the path's
+    // previous segment CTA (decoupled look-back, same launch); null: identity
+    const bool lookback = g.pub != nullptr && sg > 0;
+    const float* __restrict__ pre0 = lookback ? g.pub + (b * g.G + sg - 1) * D : nullptr;
     const int U = g.U, UP = g.UP, CL = g.CL;
     const int tid = threadIdx.x, nth = blockDim.x;
     const float* __restrict__ xb = X + b * L * d;
@@ -158,7 +160,18 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
     // ---- true prefixes P^(j), j = 0..U-1, all levels
     CombineSmem<d, N, P1S> S(reinterpret_cast<float*>(area), U);
     float* top = reinterpret_cast<float*>(area) + CLY::floats(U, 0);  // [U+1][LNP]: P^(j)_N
-    if (pre0 != nullptr) pdl_wait();  // the prefix rows come from the previous launch
+    if (lookback) {  // wait for the previous segment of this path (same launch)
+        if (tid == 0) {
+            const int* f = g.flags + b * g.G + sg - 1;
+            int v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                if (v == g.epoch) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+    }
     if (active) store_low_levels<PF, 1>(st, k, pre, S.ylow);
     if (tid < d) S.p10[tid] = __ldg(xb + seg0 * d + tid) - __ldg(xb + tid);  // P^(0)_1 = X[seg0] - X[0] (raw is dead)
     S.p0 = pre0;                                            // P^(0), levels 2..N-1 (null: zero)
@@ -187,7 +200,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
     }
     __syncthreads();
     for (int F = tid; F < LN; F += nth) {  // exclusive scan over chunks, fixed order
-        float run = pre0 != nullptr ? __ldcg(pre0 + DL + F) : 0.f;  // P^(0)_N (a previous launch's output: via L2)
+        float run = pre0 != nullptr ? __ldcg(pre0 + DL + F) : 0.f;  // P^(0)_N (another CTA's output: via L2)
         top[F] = run;
         for (int j = 1; j <= U; ++j) {
             run += top[(size_t)j * LNP + F];
@@ -195,6 +208,18 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
         }
     }
     __syncthreads();
+    if (g.pub != nullptr && sg + 1 < g.G) {
+        // publish P^(U) = signature of X[0 .. segment end] for the next segment CTA;
+        // the previous launch is complete first (it may still read these rows)
+        pdl_wait();
+        float* prow = g.pub + (b * g.G + sg) * D;
+        const float* pU = S.pf + (size_t)U * DL;
+        for (int i = tid; i < DL; i += nth) prow[i] = pU[i];
+        for (int F = tid; F < LN; F += nth) prow[DL + F] = top[(size_t)U * LNP + F];
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(g.flags + b * g.G + sg), "r"(g.epoch) : "memory");
+    }
     // ---- pass 2: fold every chunk again from its true prefix, streaming rows
 #pragma unroll
     for (int i = 0; i < PF::S; ++i) st[i] = 0;

@@ -185,7 +185,7 @@ struct PairVariant {
     static constexpr auto skernel = pair_stream_kernel<DIM, DEPTH, Q, NT, MINB>;
     static std::atomic<uint64_t> ssmem_done;
     static cudaError_t stream_launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s,
-                                     bool overlap, int G, const void* prefix) {
+                                     bool overlap, int G, void* pub, int* flags, int epoch) {
         const int64_t M = L - 1;
         G = std::max(1, G);
         const int64_t SL = (M + G - 1) / G;
@@ -208,28 +208,17 @@ struct PairVariant {
         g.CL = CL;
         g.threads = threads(U);
         g.raw_floats = raw_floats(SL);
-        g.prefix = G > 1 ? static_cast<const float*>(prefix) : nullptr;
+        g.pub = G > 1 ? static_cast<float*>(pub) : nullptr;
+        g.flags = flags;
+        g.epoch = epoch;
         return launch_maybe_overlapped(skernel, dim3((unsigned)(B * G)), dim3(g.threads), sm, s, overlap,
                                        static_cast<const float*>(X), L, g, TS, static_cast<float*>(out));
-    }
-    static constexpr auto pkernel = segment_prefix_kernel<DIM, DEPTH, (DIM > 1 && DEPTH > 1)>;
-    static std::atomic<uint64_t> psmem_done;
-    static cudaError_t prefix_launch(const void* rows, int64_t B, int G, void* prefix, cudaStream_t s) {
-        using CLY = CombineLayout<DIM, DEPTH>;
-        const size_t sm = (CLY::floats(G, 0) + (size_t)G * CLY::LN) * 4;
-        if (sm > 227 * 1024) return cudaErrorInvalidValue;
-        cudaError_t e = opt_in_smem(pkernel, sm, psmem_done);
-        if (e != cudaSuccess) return e;
-        return launch_maybe_overlapped(pkernel, dim3((unsigned)B), dim3(256), sm, s, true,
-                                       static_cast<const float*>(rows), G, static_cast<float*>(prefix));
     }
 };
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::smem_done{0};
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::ssmem_done{0};
-template <int DIM, int DEPTH, int Q>
-std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::psmem_done{0};
 
 // Smallest Q whose pair state (two chunks) fits ~80 registers, or -1.
 constexpr int pick_q_pair(int d, int N) {
@@ -253,7 +242,6 @@ Variant make_pair_variant() {
     v.pair_occupancy = &V::occupancy;
     v.pair_units_max = V::NT / PF::P;
     v.stream_launch = &V::stream_launch;
-    v.prefix_launch = &V::prefix_launch;
     return v;
 }
 

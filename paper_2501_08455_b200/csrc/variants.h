@@ -49,12 +49,11 @@ struct Variant {
     cudaError_t (*pair_launch)(const PairLaunch& a);
     cudaError_t (*pair_occupancy)(int U, int CL, int64_t SL, int G, int* blocks_per_sm);  // 0: does not fit
     int pair_units_max;  // max U/2 per CTA
-    // pair family: prefix stream (B, L-1, D); G segments per path (CTA (b, g) starts from prefix row
-    // b*G + g, null for G == 1); cudaErrorInvalidValue when a segment does not fit one CTA
+    // pair family: prefix stream (B, L-1, D); G segments per path, CTA (b, g) starting from the row its
+    // predecessor segment publishes in the same launch (pub/flags/epoch); cudaErrorInvalidValue when a
+    // segment does not fit one CTA
     cudaError_t (*stream_launch)(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, bool overlap,
-                                 int G, const void* prefix);
-    // pair family: exclusive prefix products of (B*G, D) segment rows -> (B*G, D) prefix rows
-    cudaError_t (*prefix_launch)(const void* rows, int64_t B, int G, void* prefix, cudaStream_t s);
+                                 int G, void* pub, int* flags, int epoch);
 };
 
 const Variant* find_variant(int d, int N, bool is_f64);  // first (smallest-Q) candidate
