@@ -40,7 +40,19 @@ void validate_depth(int depth) {
     if (depth < 1) throw DomainError("depth must be >= 1, got " + std::to_string(depth));
 }
 
-SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats) {
+// KernelStats keep the reference's observable meaning (kernels.cpp:106-148,
+// sig_core.hpp:194-204): the sequential-stage count of the reference
+// algorithm of the selected kind — fold_steps = L-1 for the sequential kernel,
+// scan_passes = depth for the parallel one. The GPU decomposition (chunks,
+// segments, launches) is reported by the C ABI's sigk_stats.
+void ref_counters(KernelKind kind, std::size_t len, int depth, KernelStats* stats) {
+    if (!stats) return;
+    const bool par = kind == KernelKind::Parallel;
+    stats->fold_steps = par ? 0 : static_cast<std::int64_t>(len) - 1;
+    stats->scan_passes = par ? depth : 0;
+}
+
+SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats, KernelKind kind) {
     validate_paths(paths);
     validate_depth(depth);
     SignatureBatch out;
@@ -51,10 +63,7 @@ SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats) {
     sigk_stats st{};
     check(sigk_signature_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, out.flat.data(), 0u,
                              nullptr, nullptr, &st));
-    if (stats) {
-        stats->fold_steps = st.fold_steps;
-        stats->scan_passes = st.scan_passes;
-    }
+    ref_counters(kind, paths.len, depth, stats);
     return out;
 }
 
@@ -124,7 +133,6 @@ PrefixSignatureBatch signature_stream(const PathBatch& paths, int depth, KernelK
     validate_depth(depth);
     if (paths.len < 2)
         throw DomainError("signature_stream: need at least 2 points, got L = " + std::to_string(paths.len));
-    (void)select_kernel(kernel, caps, paths.len);  // accepted for source compatibility (kernels.cpp:165)
     PrefixSignatureBatch out;
     out.batch = paths.batch;
     out.prefixes = paths.len - 1;
@@ -134,10 +142,7 @@ PrefixSignatureBatch signature_stream(const PathBatch& paths, int depth, KernelK
     sigk_stats st{};
     check(sigk_signature_stream_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, out.flat.data(), 0u,
                                     nullptr, nullptr, &st));
-    if (stats) {
-        stats->fold_steps = st.fold_steps;
-        stats->scan_passes = st.scan_passes;
-    }
+    ref_counters(select_kernel(kernel, caps, paths.len), paths.len, depth, stats);
     return out;
 }
 
@@ -234,7 +239,7 @@ ScaledIncrements scaled_increments(const IncrementBatch& inc, int depth) {
 }
 
 SignatureBatch signature_sequential(const PathBatch& paths, int depth, KernelStats* stats) {
-    return run_gpu(paths, depth, stats);
+    return run_gpu(paths, depth, stats, KernelKind::Sequential);
 }
 
 SignatureBatch signature_parallel(const PathBatch& paths, int depth, KernelStats* stats, std::size_t memory_cap) {
@@ -248,24 +253,20 @@ SignatureBatch signature_parallel(const PathBatch& paths, int depth, KernelStats
         throw ResourceError("parallel kernel: intermediate storage of ~" + std::to_string(static_cast<double>(scalars)) +
                             " scalars exceeds cap " + std::to_string(memory_cap) +
                             "; use the sequential kernel for this shape");
-    return run_gpu(paths, depth, stats);
+    return run_gpu(paths, depth, stats, KernelKind::Parallel);
 }
 
 SignatureBatch signature(const PathBatch& paths, int depth, KernelKind kernel, const ExecutionCaps& caps,
                          KernelStats* stats) {
     validate_paths(paths);
-    (void)select_kernel(kernel, caps, paths.len);
-    return run_gpu(paths, depth, stats);
+    return run_gpu(paths, depth, stats, select_kernel(kernel, caps, paths.len));
 }
 
 void signature_f32(const float* paths, std::size_t batch, std::size_t len, int dim, int depth, float* out,
                    KernelStats* stats) {
     sigk_stats st{};
     check(sigk_signature_f32(paths, batch, len, dim, depth, out, 0u, nullptr, nullptr, &st));
-    if (stats) {
-        stats->fold_steps = st.fold_steps;
-        stats->scan_passes = st.scan_passes;
-    }
+    ref_counters(KernelKind::Sequential, len, depth, stats);  // the float core is sequential_forward<float>
 }
 
 // ---- tensor algebra (host utilities; semantics of tensor_algebra.cpp:10-127)

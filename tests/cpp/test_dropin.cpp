@@ -118,7 +118,11 @@ int main() {
         for (double v : ref.flat) scale = std::fmax(scale, std::fabs(v));
         std::vector<double> o(out.begin(), out.end());
         CHECK(max_abs_diff(o, ref.flat) <= 1e-5 * scale);
-        CHECK(st.fold_steps >= 1);
+        CHECK(st.fold_steps == 999 && st.scan_passes == 0);  // reference counters (kernels.cpp:106-122)
+        KernelStats sp, ss;
+        signature_parallel(random_paths(8, 2, 50, 2, 0.3), 3, &sp);
+        signature_sequential(random_paths(8, 2, 50, 2, 0.3), 3, &ss);
+        CHECK(sp.fold_steps == 0 && sp.scan_passes == 3 && ss.fold_steps == 49 && ss.scan_passes == 0);
     }
 
     // test_kernels.cpp:334-346 — invalid shapes and depths, exception classes
