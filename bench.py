@@ -82,7 +82,7 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.h = nvml_handle(pynvml, index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception:
@@ -116,6 +116,19 @@ class ClockSampler:
         return {"sm_mhz": s[len(s) // 2], "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(s)}
 
 
+def nvml_handle(pynvml, cuda_index):
+    """NVML handle of a CUDA device by PCI bus id (NVML and CUDA orders can differ,
+    e.g. under CUDA_VISIBLE_DEVICES); falls back to the index."""
+    try:
+        import torch
+
+        pr = torch.cuda.get_device_properties(cuda_index)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        return pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+    except Exception:
+        return pynvml.nvmlDeviceGetHandleByIndex(cuda_index)
+
+
 def bind_to_gpu_numa(index):
     """Run on the host cores local to the GPU (NVML CPU affinity) so pinned
     host buffers are first-touched on the GPU's NUMA node: the e2e copies then
@@ -124,7 +137,7 @@ def bind_to_gpu_numa(index):
         import pynvml
 
         pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        h = nvml_handle(pynvml, index)
         words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
         cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
         cpus &= set(range(os.cpu_count()))
@@ -282,7 +295,7 @@ def run_ours(args):
         g_main.replay()
     torch.cuda.synchronize()
 
-    clk = ClockSampler(torch.cuda.current_device() if world == 1 else local)
+    clk = ClockSampler(torch.cuda.current_device())
     barrier(world)
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
