@@ -31,7 +31,7 @@ def rel(a, b):
     return float(np.max(np.abs(a - b)) / max(1e-30, np.max(np.abs(b))))
 
 
-@pytest.mark.parametrize("B,L,d,N", [(2, 2, 3, 3), (3, 7, 2, 4), (2, 33, 3, 3), (2, 50, 5, 4), (1, 20, 1, 5),
+@pytest.mark.parametrize("B,L,d,N", [(2, 2, 3, 3), (3, 7, 2, 4), (2, 33, 3, 3), (2, 50, 5, 4), (1, 20, 1, 5), (2, 40, 10, 3), (5, 70, 4, 4), (3, 64, 6, 3),
                                      (2, 12, 4, 2), (2, 9, 2, 1)])
 def test_vjp_f64_matches_reference(sk, B, L, d, N):
     X = walk(B, L, d, seed=B * 100 + L)
