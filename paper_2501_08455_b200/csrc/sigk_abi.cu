@@ -1006,8 +1006,15 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     auto release = [&] {
         for (void* q : tmp) cudaFreeAsync(q, s);
     };
+    // slice-parallel adjoint where a prefix length fits a warp: it walks the
+    // states back by inverse steps from the chunk ends, so no per-step state is
+    // stored; otherwise the element-parallel kernel reads every prefix state
+    VjpSlice<Real> sl;
+    if constexpr (sizeof(Real) == 4) sl = vjp_slice_for_f32(d, N);
+    else sl = vjp_slice_for_f64(d, N);
+    if (getenv("SIGK_VJP_ELEMENT")) sl.fn = nullptr;  // experiments: the element-parallel kernel
     Real* states = nullptr;
-    if (M > 0) {
+    if (M > 0 && !sl.fn) {
         e = alloc(reinterpret_cast<void**>(&states), sizeof(Real) * B * M * D);
         if (e != cudaSuccess) return cuda_fail(e, "vjp state allocation");
         const int rc = stream_device<Real>(X, B, L, d, N, states, s, tun, st);
@@ -1030,6 +1037,21 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     if (M > 0) U = (int)((M + CL - 1) / CL);
     int launches = 0;
     const Real* cbars = cot;
+    Real* ends = nullptr;  // slice path: forward prefix at every chunk end
+    if (U == 1 && M > 0 && sl.fn) {
+        e = alloc(reinterpret_cast<void**>(&ends), sizeof(Real) * B * D);
+        if (e != cudaSuccess) {
+            release();
+            return cuda_fail(e, "vjp allocation");
+        }
+        sigk_stats cst{};
+        const int rc = run_device<Real>(X, B, L, d, N, ends, s, nullptr, &cst);  // one chunk: the signature
+        if (rc != SIGK_OK) {
+            release();
+            return rc;
+        }
+        launches += cst.launches;
+    }
     if (U > 1) {
         Real *Xseg = nullptr, *C = nullptr, *cb = nullptr;
         e = alloc(reinterpret_cast<void**>(&Xseg), sizeof(Real) * B * U * (CL + 1) * d);
@@ -1052,6 +1074,16 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         vjp_boundary_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, cot, cb, U, d, N, D);
         cbars = cb;
         launches += 2 + cst.launches;
+        if (sl.fn) {
+            if ((e = alloc(reinterpret_cast<void**>(&ends), sizeof(Real) * B * U * D)) != cudaSuccess) {
+                release();
+                return cuda_fail(e, "vjp allocation");
+            }
+            if (bsm > 48 * 1024)
+                cudaFuncSetAttribute(vjp_ends_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
+            vjp_ends_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, U, d, N, D, ends);
+            launches += 1;
+        }
     }
     Real* dbar = nullptr;
     if (M > 0 && (e = alloc(reinterpret_cast<void**>(&dbar), sizeof(Real) * B * M * d)) != cudaSuccess) {
@@ -1072,10 +1104,6 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     if constexpr (sizeof(Real) == 4) vk = vjp_kernel_for_f32(d, N);
     else vk = vjp_kernel_for_f64(d, N);
     if (use_smem && work > 48 * 1024) cudaFuncSetAttribute(vk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)work);
-    VjpSlice<Real> sl;
-    if constexpr (sizeof(Real) == 4) sl = vjp_slice_for_f32(d, N);
-    else sl = vjp_slice_for_f64(d, N);
-    if (getenv("SIGK_VJP_ELEMENT")) sl.fn = nullptr;  // experiments: the element-parallel kernel
     if (M > 0 && sl.fn) {
         // slice-parallel adjoint: SLOTS (path, chunk) items per warp, 4 warps per CTA
         const int64_t items = B * U, per_cta = 4 * (int64_t)sl.slots;
@@ -1088,7 +1116,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, sl.fn, X, L, items, U, CL, static_cast<const Real*>(states), cbars, dbar);
+        e = cudaLaunchKernelEx(&cfg, sl.fn, X, L, items, U, CL, static_cast<const Real*>(ends), cbars, dbar);
         if (e != cudaSuccess) {
             release();
             return cuda_fail(e, "vjp slice launch");

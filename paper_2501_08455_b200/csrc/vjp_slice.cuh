@@ -170,6 +170,50 @@ struct SliceRev {
     }
 };
 
+// One Horner step S <- S ⊠ exp(δ) on a lane's slice (levels descending, so
+// lower levels are still the old state): the slice-local fold of the forward
+// kernels in scalar form. With -δ it undoes a step (exp(-δ) is the inverse of
+// exp(δ)), which is how the backward walk recovers the states it needs.
+template <typename Real, int d, int N, int Q>
+struct SliceFold {
+    using LY = SliceLayout<d, N, Q>;
+    static constexpr int S = LY::S, NLOW = LY::NLOW, VS = LY::VS;
+    __device__ __forceinline__ static Real& sc(Real (&v)[S], int k) { return k < Q ? v[k - 1] : v[NLOW]; }
+    template <int n>
+    __device__ __forceinline__ static void levels(Real (&st)[S], const Real (&dl)[d], const Real (&dp)[Q + 1]) {
+        if constexpr (n >= 1) {
+            if constexpr (n == 1) {
+                sc(st, 1) += dp[1];
+            } else {
+                Real u = dp[1] * (Real(1) / Real(n)) + sc(st, 1);
+                constexpr int kq = n - 1 < Q ? n - 1 : Q;
+#pragma unroll
+                for (int k = 2; k <= kq; ++k) u = u * dp[k] * (Real(1) / Real(n - k + 1)) + sc(st, k);
+                if constexpr (n <= Q) {
+                    sc(st, n) += u * dp[n];
+                } else {
+                    Real uv[VS];
+#pragma unroll
+                    for (int k = Q + 1; k <= n - 1; ++k) {
+                        const Real inv = Real(1) / Real(n - k + 1);
+#pragma unroll
+                        for (int J = ipow(d, k - Q) - 1; J >= 0; --J) {
+                            const Real prev = k == Q + 1 ? u : uv[LY::vo(k - 1) + J / d];
+                            uv[LY::vo(k) + J] = prev * dl[J % d] * inv + st[LY::top_off(k) + J];
+                        }
+                    }
+#pragma unroll
+                    for (int J = 0; J < ipow(d, n - Q); ++J) {
+                        const Real prev = n - 1 == Q ? u : uv[LY::vo(n - 1) + J / d];
+                        st[LY::top_off(n) + J] += prev * dl[J % d];
+                    }
+                }
+            }
+            levels<n - 1>(st, dl, dp);
+        }
+    }
+};
+
 template <typename Real, int d, int N, int Q>
 struct SliceGather {
     using LY = SliceLayout<d, N, Q>;
@@ -186,7 +230,7 @@ struct SliceGather {
 
 template <typename Real, int d, int N, int Q>
 __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__ X, int64_t L, int64_t items,
-                                                        int U, int64_t CL, const Real* __restrict__ states,
+                                                        int U, int64_t CL, const Real* __restrict__ ends,
                                                         const Real* __restrict__ cbars, Real* __restrict__ dbar) {
     using LY = SliceLayout<d, N, Q>;
     constexpr int P = LY::P, SLOTS = LY::SLOTS, S = LY::S, NLOW = LY::NLOW, VS = LY::VS, GMAX = LY::GMAX;
@@ -221,24 +265,18 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
         SliceGather<Real, d, N, Q>::template level<Q>(row, ok, lvl, dst);
     };
     const Real* xb = X + b * L * d;
-    const Real* sb = states + b * M * D;
-    auto load_state = [&](int64_t s, Real (&dst)[S]) {  // S_s = row s-1; identity (zeros) for s <= 0
-        const bool ok = valid && s >= 1 && s <= M;
-        gather(sb + (ok ? s - 1 : 0) * D, ok, dst);
-    };
     pdl_trigger();
-    pdl_wait();  // cbars and states come from the previous launches: read them through L2
+    pdl_wait();  // cbars and ends come from the previous launches: read them through L2
                  // (ld.global.cg), never through an L1 line filled while those launches ran
     gather(crow, valid, cb);
+    // the state at the chunk's end (the forward prefix, ends row), walked back
+    // one step at a time: S_s = S_{s+1} ⊠ exp(-δ_s)
+    gather(ends + it * D, valid, an);
     // scal(k): A_k / C̄_k at prefix p_1..p_k for k <= Q
     auto sc = [&](Real (&v)[S], int k) -> Real& { return k < Q ? v[k - 1] : v[NLOW]; };
-    load_state(s_hi - 1, an);
     for (int64_t st = 0; st < CL; ++st) {
         const int64_t s = s_hi - 1 - st;
         const bool on = valid && s >= s_lo;
-#pragma unroll
-        for (int i = 0; i < S; ++i) a[i] = an[i];
-        if (on) load_state(s - 1, an);  // prefetch the next (earlier) state
         Real dl[d];
 #pragma unroll
         for (int c = 0; c < d; ++c) dl[c] = on ? xb[(s + 1) * d + c] - xb[s * d + c] : Real(0);
@@ -246,6 +284,16 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
 #pragma unroll
         for (int k = 1; k <= Q; ++k)  // δ[p_k] from memory (a register array indexed by p_k would spill)
             dp[k] = on ? xb[(s + 1) * d + dg[k]] - xb[s * d + dg[k]] : Real(0);
+        {
+            Real ndl[d], ndp[Q + 1];
+#pragma unroll
+            for (int c = 0; c < d; ++c) ndl[c] = -dl[c];
+#pragma unroll
+            for (int k = 1; k <= Q; ++k) ndp[k] = -dp[k];
+            SliceFold<Real, d, N, Q>::template levels<N>(an, ndl, ndp);
+#pragma unroll
+            for (int i = 0; i < S; ++i) a[i] = s == 0 ? Real(0) : an[i];  // S_0: the identity, exactly
+        }
         Real gd[d], gk[Q + 1];
 #pragma unroll
         for (int c = 0; c < d; ++c) gd[c] = Real(0);

@@ -97,3 +97,15 @@ def test_vjp_chunked_matches_single_walk(sk, chunks):
     assert st.chunks == chunks
     assert rel(got, one) <= 1e-11
     assert rel(got, O.ref_vjp(X, 4, cot)) <= 1e-10
+
+
+@pytest.mark.parametrize("chunks", [0, 10, 2])
+def test_vjp_f32_long_chunks(sk, chunks):
+    # long chunks: the slice adjoint recovers states by inverse steps over up to 5000 steps in fp32
+    X = walk(2, 10000, 5, seed=17)
+    cot = np.random.default_rng(18).standard_normal((2, 780))
+    st = sk.KernelStats()
+    got = sk.signature_vjp(X.astype(np.float32), 4, cot.astype(np.float32), stats=st, chunks=chunks)
+    ref = O.ref_vjp(X.astype(np.float32).astype(np.float64), 4, cot.astype(np.float32).astype(np.float64))
+    print("chunks", st.chunks, "steps per chunk", st.fold_steps, "rel", rel(got, ref))
+    assert rel(got, ref) <= 1e-4, rel(got, ref)
