@@ -1069,20 +1069,30 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             return rc;
         }
         const size_t bsm = 3 * sizeof(Real) * (size_t)D;
-        if (bsm > 48 * 1024)
-            cudaFuncSetAttribute(vjp_boundary_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
-        vjp_boundary_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, cot, cb, U, d, N, D);
         cbars = cb;
-        launches += 2 + cst.launches;
+        launches += 1 + cst.launches;
         if (sl.fn) {
             if ((e = alloc(reinterpret_cast<void**>(&ends), sizeof(Real) * B * U * D)) != cudaSuccess) {
                 release();
                 return cuda_fail(e, "vjp allocation");
             }
+        }
+        if (sl.fn && sl.passes) {  // compile-time shape: boundary and ends in one pass per path
             if (bsm > 48 * 1024)
-                cudaFuncSetAttribute(vjp_ends_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
-            vjp_ends_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, U, d, N, D, ends);
+                cudaFuncSetAttribute(sl.passes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
+            sl.passes<<<(unsigned)B, 256, bsm, s>>>(C, cot, U, cb, ends);
             launches += 1;
+        } else {
+            if (bsm > 48 * 1024)
+                cudaFuncSetAttribute(vjp_boundary_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
+            vjp_boundary_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, cot, cb, U, d, N, D);
+            launches += 1;
+            if (sl.fn) {
+                if (bsm > 48 * 1024)
+                    cudaFuncSetAttribute(vjp_ends_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
+                vjp_ends_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, U, d, N, D, ends);
+                launches += 1;
+            }
         }
     }
     Real* dbar = nullptr;

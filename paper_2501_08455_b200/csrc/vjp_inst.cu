@@ -32,6 +32,7 @@ static void slice_case(int d, int N, VjpSlice<Real>& out) {
         if (d == DD && N == NN) {
             out.fn = vjp_slice_kernel<Real, DD, NN, Q>;
             out.slots = SliceLayout<DD, NN, Q>::SLOTS;
+            out.passes = vjp_chunk_passes_kernel<Real, DD, NN>;
         }
     }
 }

@@ -377,4 +377,98 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
     }
 }
 
+// Compile-time (d, N) forms of the per-path chunk passes (vjp_kernel.cuh:
+// vjp_boundary_kernel / vjp_ends_kernel): same arithmetic in the same order,
+// with constant level offsets and divisors so the index math folds away.
+template <typename Real, int d, int N>
+struct ChunkPasses {
+    static constexpr int D = level_off(d, N);
+    __device__ __forceinline__ static int off(int n) { return level_off(d, n); }
+    // nxt = cur pulled back through right multiplication by sig (the adjoint)
+    template <int n>
+    __device__ __forceinline__ static void adjoint(const Real* __restrict__ cur, const Real* __restrict__ sig,
+                                                   Real* __restrict__ nxt) {
+        if constexpr (n <= N) {
+            for (int I = threadIdx.x; I < ipow(d, n); I += blockDim.x) {
+                Real acc = cur[off(n - 1) + I];
+#pragma unroll
+                for (int k = 1; n + k <= N; ++k) {
+                    const Real* cr = cur + off(n + k - 1) + I * ipow(d, k);
+                    const Real* er = sig + off(k - 1);
+#pragma unroll 5
+                    for (int J = 0; J < ipow(d, k); ++J) acc = fma(cr[J], er[J], acc);
+                }
+                nxt[off(n - 1) + I] = acc;
+            }
+            adjoint<n + 1>(cur, sig, nxt);
+        }
+    }
+    // nxt = cur ⊠ sig (Chen product)
+    template <int n>
+    __device__ __forceinline__ static void product(const Real* __restrict__ cur, const Real* __restrict__ sig,
+                                                   Real* __restrict__ nxt) {
+        if constexpr (n <= N) {
+            for (int I = threadIdx.x; I < ipow(d, n); I += blockDim.x) {
+                Real v = cur[off(n - 1) + I] + sig[off(n - 1) + I];
+#pragma unroll
+                for (int a = 1; a < n; ++a) {
+                    const int tail = ipow(d, n - a);
+                    v = fma(cur[off(a - 1) + I / tail], sig[off(n - a - 1) + I % tail], v);
+                }
+                nxt[off(n - 1) + I] = v;
+            }
+            product<n + 1>(cur, sig, nxt);
+        }
+    }
+};
+
+// boundary + ends in one pass per path: cbars rows (cotangent at every chunk
+// end, backwards from the output cotangent) and ends rows (forward prefix at
+// every chunk end), dynamic shared memory 4 D
+template <typename Real, int d, int N>
+__global__ void __launch_bounds__(256) vjp_chunk_passes_kernel(const Real* __restrict__ C, const Real* __restrict__ cot,
+                                                               int U, Real* __restrict__ cbars, Real* __restrict__ ends) {
+    using CP = ChunkPasses<Real, d, N>;
+    constexpr int D = CP::D;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* cur = reinterpret_cast<Real*>(smem_raw);
+    Real* sig = cur + D;
+    Real* nxt = sig + D;
+    const int64_t b = blockIdx.x;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    pdl_trigger();
+    pdl_wait();
+    // forward: ends[j] = C_0 ⊠ ... ⊠ C_j
+    for (int i = tid; i < D; i += nth) cur[i] = Real(0);
+    __syncthreads();
+    for (int j = 0; j < U; ++j) {
+        for (int i = tid; i < D; i += nth) sig[i] = __ldcg(C + (b * U + j) * D + i);
+        __syncthreads();
+        CP::template product<1>(cur, sig, nxt);
+        __syncthreads();
+        for (int i = tid; i < D; i += nth) {
+            cur[i] = nxt[i];
+            ends[(b * U + j) * D + i] = nxt[i];
+        }
+        __syncthreads();
+    }
+    // backward: cbars[U-1] = cot, cbars[j-1] = cbars[j] pulled back through C_j
+    for (int i = tid; i < D; i += nth) {
+        const Real v = __ldcg(cot + b * D + i);
+        cur[i] = v;
+        cbars[(b * U + U - 1) * D + i] = v;
+    }
+    for (int j = U - 1; j >= 1; --j) {
+        for (int i = tid; i < D; i += nth) sig[i] = __ldcg(C + (b * U + j) * D + i);
+        __syncthreads();
+        CP::template adjoint<1>(cur, sig, nxt);
+        __syncthreads();
+        for (int i = tid; i < D; i += nth) {
+            cur[i] = nxt[i];
+            cbars[(b * U + j - 1) * D + i] = nxt[i];
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace sigk
