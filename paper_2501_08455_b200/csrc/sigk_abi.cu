@@ -1077,7 +1077,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
                 return cuda_fail(e, "vjp allocation");
             }
         }
-        if (sl.fn && sl.passes) {  // compile-time shape: boundary and ends in one pass per path
+        if (sl.fn) {  // slice shapes: boundary and ends in one compile-time pass per path
             if (bsm > 48 * 1024)
                 cudaFuncSetAttribute(sl.passes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
             sl.passes<<<(unsigned)B, 256, bsm, s>>>(C, cot, U, cb, ends);
@@ -1087,12 +1087,6 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
                 cudaFuncSetAttribute(vjp_boundary_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
             vjp_boundary_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, cot, cb, U, d, N, D);
             launches += 1;
-            if (sl.fn) {
-                if (bsm > 48 * 1024)
-                    cudaFuncSetAttribute(vjp_ends_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
-                vjp_ends_kernel<Real><<<(unsigned)B, 256, bsm, s>>>(C, U, d, N, D, ends);
-                launches += 1;
-            }
         }
     }
     Real* dbar = nullptr;

@@ -312,56 +312,6 @@ __global__ void __launch_bounds__(256) vjp_boundary_kernel(const Real* __restric
     }
 }
 
-// Forward prefixes at every chunk end, one CTA per path: ends row j =
-// C_0 ⊠ ... ⊠ C_j (Chen products of the chunk signatures, tensor_algebra.cpp:80-102),
-// the state the slice adjoint starts each chunk's backward walk from.
-template <typename Real>
-__global__ void __launch_bounds__(256) vjp_ends_kernel(const Real* __restrict__ C, int U, int d, int N, int64_t D,
-                                                       Real* __restrict__ ends) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Real* cur = reinterpret_cast<Real*>(smem_raw);
-    Real* sig = cur + D;
-    Real* nxt = sig + D;
-    __shared__ int64_t off[kGenericMaxDepth + 1];
-    __shared__ int64_t pw[kGenericMaxDepth + 1];
-    const int64_t b = blockIdx.x;
-    const int tid = threadIdx.x, nth = blockDim.x;
-    if (tid == 0) {
-        off[0] = 0;
-        pw[0] = 1;
-        for (int n = 1; n <= N; ++n) {
-            pw[n] = pw[n - 1] * d;
-            off[n] = off[n - 1] + pw[n];
-        }
-    }
-    pdl_trigger();
-    pdl_wait();
-    for (int64_t i = tid; i < D; i += nth) cur[i] = Real(0);  // the identity
-    __syncthreads();
-    for (int j = 0; j < U; ++j) {
-        const Real* cj = C + (b * U + j) * D;
-        for (int64_t i = tid; i < D; i += nth) sig[i] = __ldcg(cj + i);
-        __syncthreads();
-        for (int64_t q = tid; q < D; q += nth) {
-            int n = 1;
-            while (q >= off[n]) ++n;
-            const int64_t I = q - off[n - 1];
-            Real v = cur[q] + sig[q];
-            for (int a = 1; a < n; ++a) {
-                const int64_t tail = pw[n - a];
-                v = fma(cur[off[a - 1] + I / tail], sig[off[n - a - 1] + I % tail], v);
-            }
-            nxt[q] = v;
-        }
-        __syncthreads();
-        for (int64_t i = tid; i < D; i += nth) {
-            cur[i] = nxt[i];
-            ends[(b * U + j) * D + i] = nxt[i];
-        }
-        __syncthreads();
-    }
-}
-
 // ∂/∂X_t = δ̄_{t-1} - δ̄_t (δ̄_{-1} = δ̄_M = 0), grad (B, L, d)
 template <typename Real>
 __global__ void vjp_grad_kernel(const Real* __restrict__ dbar, int64_t B, int64_t L, int d, Real* __restrict__ grad) {

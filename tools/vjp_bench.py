@@ -22,9 +22,14 @@ g = torch.empty_like(X)
 s = torch.cuda.current_stream()
 
 
+import os  # noqa: E402
+
+TUN = sk._Tuning(chunks=int(os.environ.get("VJP_CHUNKS", "0")))
+
+
 def call():
     sk._check(sk.lib().sigk_signature_vjp_f32(X.data_ptr(), B, L, d, N, cot.data_ptr(), g.data_ptr(), 1,
-                                              C.c_void_p(s.cuda_stream), None, None))
+                                              C.c_void_p(s.cuda_stream), C.byref(TUN), None))
 
 
 for _ in range(2):
