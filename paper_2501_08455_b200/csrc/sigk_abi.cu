@@ -1027,9 +1027,12 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     // kernels on the gathered chunks) give the cotangent at every chunk end
     const int sms = device_info([] { int v = 0; cudaGetDevice(&v); return v; }()).sms;
     int U = 1;
-    // (the boundary pass stages 3 rows of D in shared memory; wider signatures walk whole paths)
-    if (M >= 32 && (tun == nullptr || tun->chunks != 1) && 3 * sizeof(Real) * (size_t)D <= 227 * 1024) {
-        const int64_t want = ((int64_t)sms * 8 + B - 1) / B;
+    // (the boundary pass stages 3 rows of D in shared memory, the slice shapes' chunk
+    // pass at least 6; wider signatures walk whole paths)
+    if (M >= 32 && (tun == nullptr || tun->chunks != 1) && (sl.fn ? 6 : 3) * sizeof(Real) * (size_t)D <= 227 * 1024) {
+        // B*U items fill the GPU, and chunks stay <= ~250 steps (the backward walk is
+        // latency-bound per item: long paths want more, shorter items)
+        const int64_t want = std::max<int64_t>(((int64_t)sms * 8 + B - 1) / B, M / 250);
         U = (int)std::max<int64_t>(1, std::min<int64_t>(want, M / 16));
         if (tun && tun->chunks > 1) U = (int)std::min<int64_t>(tun->chunks, M);
     }
@@ -1078,9 +1081,12 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             }
         }
         if (sl.fn) {  // slice shapes: boundary and ends in one compile-time pass per path
-            if (bsm > 48 * 1024)
-                cudaFuncSetAttribute(sl.passes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(bsm, 227 * 1024));
-            sl.passes<<<(unsigned)B, 256, bsm, s>>>(C, cot, U, cb, ends);
+            const size_t rsm = (size_t)(U + 4) * D * sizeof(Real);
+            const int resident = rsm <= 200 * 1024;
+            const size_t psm = resident ? rsm : 6 * D * sizeof(Real);
+            if (psm > 48 * 1024)
+                cudaFuncSetAttribute(sl.passes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(psm, 227 * 1024));
+            sl.passes<<<(unsigned)B, 256, psm, s>>>(C, cot, U, resident, cb, ends);
             launches += 1;
         } else {
             if (bsm > 48 * 1024)

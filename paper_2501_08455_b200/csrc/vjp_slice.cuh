@@ -274,16 +274,45 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
     gather(ends + it * D, valid, an);
     // scal(k): A_k / C̄_k at prefix p_1..p_k for k <= Q
     auto sc = [&](Real (&v)[S], int k) -> Real& { return k < Q ? v[k - 1] : v[NLOW]; };
+    // points X[s+1] (hi) and X[s] (lo) of the current step in registers (all d
+    // channels, and the lane's digit channels p_k separately: a register array
+    // indexed by p_k would go to local memory); X[s-1] is loaded one step ahead
+    Real xhi[d], xlo[d], phi[Q + 1], plo[Q + 1];
+    const bool any = valid && s_hi > s_lo;
+#pragma unroll
+    for (int c = 0; c < d; ++c) {
+        xhi[c] = any ? xb[s_hi * d + c] : Real(0);
+        xlo[c] = any ? xb[(s_hi - 1) * d + c] : Real(0);
+    }
+#pragma unroll
+    for (int k = 1; k <= Q; ++k) {
+        phi[k] = any ? xb[s_hi * d + dg[k]] : Real(0);
+        plo[k] = any ? xb[(s_hi - 1) * d + dg[k]] : Real(0);
+    }
     for (int64_t st = 0; st < CL; ++st) {
         const int64_t s = s_hi - 1 - st;
         const bool on = valid && s >= s_lo;
-        Real dl[d];
+        const bool pre_on = valid && s - 1 >= s_lo;
+        Real xnx[d], pnx[Q + 1];
 #pragma unroll
-        for (int c = 0; c < d; ++c) dl[c] = on ? xb[(s + 1) * d + c] - xb[s * d + c] : Real(0);
-        Real dp[Q + 1];
+        for (int c = 0; c < d; ++c) xnx[c] = pre_on ? xb[(s - 1) * d + c] : Real(0);
 #pragma unroll
-        for (int k = 1; k <= Q; ++k)  // δ[p_k] from memory (a register array indexed by p_k would spill)
-            dp[k] = on ? xb[(s + 1) * d + dg[k]] - xb[s * d + dg[k]] : Real(0);
+        for (int k = 1; k <= Q; ++k) pnx[k] = pre_on ? xb[(s - 1) * d + dg[k]] : Real(0);
+        Real dl[d], dp[Q + 1];
+#pragma unroll
+        for (int c = 0; c < d; ++c) dl[c] = on ? xhi[c] - xlo[c] : Real(0);
+#pragma unroll
+        for (int k = 1; k <= Q; ++k) dp[k] = on ? phi[k] - plo[k] : Real(0);
+#pragma unroll
+        for (int c = 0; c < d; ++c) {
+            xhi[c] = xlo[c];
+            xlo[c] = xnx[c];
+        }
+#pragma unroll
+        for (int k = 1; k <= Q; ++k) {
+            phi[k] = plo[k];
+            plo[k] = pnx[k];
+        }
         {
             Real ndl[d], ndp[Q + 1];
 #pragma unroll
@@ -378,35 +407,71 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
 }
 
 // Compile-time (d, N) forms of the per-path chunk passes (vjp_kernel.cuh:
-// vjp_boundary_kernel / vjp_ends_kernel): same arithmetic in the same order,
-// with constant level offsets and divisors so the index math folds away.
+// vjp_boundary_kernel is the runtime form): constant level offsets and
+// divisors so the index math folds away.
 template <typename Real, int d, int N>
 struct ChunkPasses {
     static constexpr int D = level_off(d, N);
     __device__ __forceinline__ static int off(int n) { return level_off(d, n); }
-    // nxt = cur pulled back through right multiplication by sig (the adjoint)
+    // terms in the adjoint sum of a level-n entry: Σ_{k=1}^{N-n} d^k
+    __host__ __device__ static constexpr int terms(int n) { return n >= N ? 0 : level_off(d, N - n); }
+    __host__ __device__ static constexpr bool wide(int n) { return terms(n) >= 64; }
+    // nxt = cur pulled back through right multiplication by sig (the adjoint of
+    // cur ↦ cur ⊠ sig): entry I of level n sums Σ_k Σ_J cur[n+k][I·d^k + J]·sig[k][J].
+    // Wide levels: one warp per entry, lanes split J, butterfly sum (fixed order).
     template <int n>
-    __device__ __forceinline__ static void adjoint(const Real* __restrict__ cur, const Real* __restrict__ sig,
-                                                   Real* __restrict__ nxt) {
+    __device__ __forceinline__ static void adjoint_wide(const Real* __restrict__ cur, const Real* __restrict__ sig,
+                                                        Real* __restrict__ nxt, Real* __restrict__ grow) {
         if constexpr (n <= N) {
-            for (int I = threadIdx.x; I < ipow(d, n); I += blockDim.x) {
-                Real acc = cur[off(n - 1) + I];
+            if constexpr (wide(n)) {
+                const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+                for (int I = w; I < ipow(d, n); I += nw) {
+                    Real acc = Real(0);
 #pragma unroll
-                for (int k = 1; n + k <= N; ++k) {
-                    const Real* cr = cur + off(n + k - 1) + I * ipow(d, k);
-                    const Real* er = sig + off(k - 1);
-#pragma unroll 5
-                    for (int J = 0; J < ipow(d, k); ++J) acc = fma(cr[J], er[J], acc);
+                    for (int k = 1; n + k <= N; ++k) {
+                        const Real* cr = cur + off(n + k - 1) + I * ipow(d, k);
+                        const Real* er = sig + off(k - 1);
+                        for (int J = lane; J < ipow(d, k); J += 32) acc = fma(cr[J], er[J], acc);
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    if (lane == 0) {
+                        acc += cur[off(n - 1) + I];
+                        nxt[off(n - 1) + I] = acc;
+                        grow[off(n - 1) + I] = acc;
+                    }
                 }
-                nxt[off(n - 1) + I] = acc;
             }
-            adjoint<n + 1>(cur, sig, nxt);
+            adjoint_wide<n + 1>(cur, sig, nxt, grow);
+        }
+    }
+    // narrow levels: one thread per entry
+    template <int n>
+    __device__ __forceinline__ static void adjoint_narrow(const Real* __restrict__ cur, const Real* __restrict__ sig,
+                                                          Real* __restrict__ nxt, Real* __restrict__ grow) {
+        if constexpr (n <= N) {
+            if constexpr (!wide(n)) {
+                // reversed thread order: the first warps carry the wide entries
+                for (int I = blockDim.x - 1 - threadIdx.x; I < ipow(d, n); I += blockDim.x) {
+                    Real acc = cur[off(n - 1) + I];
+#pragma unroll
+                    for (int k = 1; n + k <= N; ++k) {
+                        const Real* cr = cur + off(n + k - 1) + I * ipow(d, k);
+                        const Real* er = sig + off(k - 1);
+#pragma unroll
+                        for (int J = 0; J < ipow(d, k); ++J) acc = fma(cr[J], er[J], acc);
+                    }
+                    nxt[off(n - 1) + I] = acc;
+                    grow[off(n - 1) + I] = acc;
+                }
+            }
+            adjoint_narrow<n + 1>(cur, sig, nxt, grow);
         }
     }
     // nxt = cur ⊠ sig (Chen product)
     template <int n>
     __device__ __forceinline__ static void product(const Real* __restrict__ cur, const Real* __restrict__ sig,
-                                                   Real* __restrict__ nxt) {
+                                                   Real* __restrict__ nxt, Real* __restrict__ grow) {
         if constexpr (n <= N) {
             for (int I = threadIdx.x; I < ipow(d, n); I += blockDim.x) {
                 Real v = cur[off(n - 1) + I] + sig[off(n - 1) + I];
@@ -416,58 +481,77 @@ struct ChunkPasses {
                     v = fma(cur[off(a - 1) + I / tail], sig[off(n - a - 1) + I % tail], v);
                 }
                 nxt[off(n - 1) + I] = v;
+                grow[off(n - 1) + I] = v;
             }
-            product<n + 1>(cur, sig, nxt);
+            product<n + 1>(cur, sig, nxt, grow);
         }
     }
 };
 
-// boundary + ends in one pass per path: cbars rows (cotangent at every chunk
+// Boundary + ends in one pass per path: cbars rows (cotangent at every chunk
 // end, backwards from the output cotangent) and ends rows (forward prefix at
-// every chunk end), dynamic shared memory 4 D
+// every chunk end). The forward scan and the backward pull-back are
+// independent chains, so step t does forward product t and backward
+// pull-back U-1-t together (one barrier per step). resident != 0: all U chunk
+// signatures are staged in shared memory up front ((U + 4) D values);
+// otherwise each step stages its two rows ((4 + 2) D values).
 template <typename Real, int d, int N>
 __global__ void __launch_bounds__(256) vjp_chunk_passes_kernel(const Real* __restrict__ C, const Real* __restrict__ cot,
-                                                               int U, Real* __restrict__ cbars, Real* __restrict__ ends) {
+                                                               int U, int resident, Real* __restrict__ cbars,
+                                                               Real* __restrict__ ends) {
     using CP = ChunkPasses<Real, d, N>;
     constexpr int D = CP::D;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Real* cur = reinterpret_cast<Real*>(smem_raw);
-    Real* sig = cur + D;
-    Real* nxt = sig + D;
+    Real* curF = reinterpret_cast<Real*>(smem_raw);
+    Real* nxtF = curF + D;
+    Real* curB = nxtF + D;
+    Real* nxtB = curB + D;
+    Real* sigs = nxtB + D;  // resident: [U][D]; else [2][D]
     const int64_t b = blockIdx.x;
     const int tid = threadIdx.x, nth = blockDim.x;
+    const Real* Cb = C + b * U * D;
     pdl_trigger();
     pdl_wait();
-    // forward: ends[j] = C_0 ⊠ ... ⊠ C_j
-    for (int i = tid; i < D; i += nth) cur[i] = Real(0);
-    __syncthreads();
-    for (int j = 0; j < U; ++j) {
-        for (int i = tid; i < D; i += nth) sig[i] = __ldcg(C + (b * U + j) * D + i);
-        __syncthreads();
-        CP::template product<1>(cur, sig, nxt);
-        __syncthreads();
-        for (int i = tid; i < D; i += nth) {
-            cur[i] = nxt[i];
-            ends[(b * U + j) * D + i] = nxt[i];
+    if (resident) {  // the predecessor's rows: L2, not L1; 16-byte loads when aligned
+        const size_t bytes = (size_t)U * D * sizeof(Real);
+        if (bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(Cb) & 15) == 0) {
+            const int4* src = reinterpret_cast<const int4*>(Cb);
+            int4* dst = reinterpret_cast<int4*>(sigs);
+            const int n16 = (int)(bytes / 16);
+#pragma unroll 8
+            for (int i = tid; i < n16; i += nth) dst[i] = __ldcg(src + i);
+        } else {
+            for (int i = tid; i < U * D; i += nth) sigs[i] = __ldcg(Cb + i);
         }
-        __syncthreads();
     }
-    // backward: cbars[U-1] = cot, cbars[j-1] = cbars[j] pulled back through C_j
     for (int i = tid; i < D; i += nth) {
         const Real v = __ldcg(cot + b * D + i);
-        cur[i] = v;
+        curF[i] = Real(0);
+        curB[i] = v;
         cbars[(b * U + U - 1) * D + i] = v;
     }
-    for (int j = U - 1; j >= 1; --j) {
-        for (int i = tid; i < D; i += nth) sig[i] = __ldcg(C + (b * U + j) * D + i);
-        __syncthreads();
-        CP::template adjoint<1>(cur, sig, nxt);
-        __syncthreads();
-        for (int i = tid; i < D; i += nth) {
-            cur[i] = nxt[i];
-            cbars[(b * U + j - 1) * D + i] = nxt[i];
+    for (int t = 0; t < U; ++t) {
+        const int jb = U - 1 - t;  // backward: cbars[jb-1] = cbars[jb] pulled back through C_jb
+        const Real *sF = sigs + (size_t)t * D, *sB = sigs + (size_t)jb * D;
+        if (!resident) {
+            for (int i = tid; i < D; i += nth) {
+                sigs[i] = __ldcg(Cb + (size_t)t * D + i);
+                if (jb >= 1) sigs[D + i] = __ldcg(Cb + (size_t)jb * D + i);
+            }
+            sF = sigs;
+            sB = sigs + D;
         }
         __syncthreads();
+        if (jb >= 1) CP::template adjoint_wide<1>(curB, sB, nxtB, cbars + (b * U + jb - 1) * D);
+        CP::template product<1>(curF, sF, nxtF, ends + (b * U + t) * D);
+        if (jb >= 1) CP::template adjoint_narrow<1>(curB, sB, nxtB, cbars + (b * U + jb - 1) * D);
+        __syncthreads();
+        Real* x = curF;
+        curF = nxtF;
+        nxtF = x;
+        x = curB;
+        curB = nxtB;
+        nxtB = x;
     }
 }
 
