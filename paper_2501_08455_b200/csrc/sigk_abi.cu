@@ -1064,7 +1064,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             release();
             return cuda_fail(e, "vjp chunk allocation");
         }
-        segment_gather_kernel<Real><<<sms * 8, 256, 0, s>>>(X, B, L, d, U, CL, Xseg);
+        segment_gather_kernel<Real><<<(unsigned)std::min<int64_t>(B * U, (int64_t)sms * 16), 128, 0, s>>>(X, B, L, d, U, CL, Xseg);
         sigk_stats cst{};
         const int rc = run_device<Real>(Xseg, B * U, CL + 1, d, N, C, s, nullptr, &cst);
         if (rc != SIGK_OK) {

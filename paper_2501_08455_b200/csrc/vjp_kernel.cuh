@@ -244,11 +244,17 @@ VjpSlice<double> vjp_slice_for_f64(int d, int N);
 template <typename Real>
 __global__ void segment_gather_kernel(const Real* __restrict__ X, int64_t B, int64_t L, int d, int U, int64_t CL,
                                       Real* __restrict__ Xseg) {
-    const int64_t per = (CL + 1) * d, n = B * U * per;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / per, q = i - r * per, b = r / U, j = r - b * U;
-        const int64_t t = j * CL + q / d, c = q - (q / d) * d;
-        Xseg[i] = X[(b * L + (t < L - 1 ? t : L - 1)) * d + c];
+    // chunk (b, j) is the contiguous run of points j*CL .. j*CL+CL of path b
+    // (the last point repeated past the path's end): a row copy per chunk
+    const int per = (int)((CL + 1) * d);
+    for (int64_t r = blockIdx.x; r < B * U; r += gridDim.x) {
+        const int64_t b = r / U, j = r - b * U;
+        const Real* __restrict__ src = X + (b * L + j * CL) * d;
+        const Real* __restrict__ last = X + (b * L + L - 1) * d;
+        const int64_t left = (L - j * CL) * d;
+        const int valid = left < per ? (int)left : per;
+        Real* __restrict__ dst = Xseg + r * per;
+        for (int q = threadIdx.x; q < per; q += blockDim.x) dst[q] = q < valid ? src[q] : last[q % d];
     }
 }
 
