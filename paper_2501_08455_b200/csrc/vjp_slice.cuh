@@ -335,6 +335,17 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
 #pragma unroll
         for (int J = 0; J < GMAX; ++J) ab[LY::top_off(N) + J] = cb[LY::top_off(N) + J];
         Real gq[Q + 1];  // G_Q of the targets m < Q (scalar per lane)
+        // the first Horner stage (level N-1) contracts C̄_N with δ for every target m;
+        // only its 1/(N-m) factor depends on m, so the contraction is shared
+        constexpr int H = ipow(d, N - 1 - Q);
+        Real h[H];
+#pragma unroll
+        for (int J = 0; J < H; ++J) {
+            Real acc = Real(0);
+#pragma unroll
+            for (int c = 0; c < d; ++c) acc += cb[LY::top_off(N) + J * d + c] * dl[c];
+            h[J] = acc;
+        }
 #pragma unroll
         for (int m = N - 1; m >= 1; --m) {
             // Horner down to level max(m, Q) inside the slice
@@ -349,8 +360,12 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
 #pragma unroll
                     for (int J = 0; J < ipow(d, l - Q); ++J) {
                         Real acc = Real(0);
+                        if (l == N - 1) {
+                            acc = h[J];
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < d; ++c) acc += ((N - 1 - l) % 2 == 0 ? g0[J * d + c] : g1[J * d + c]) * dl[c];
+                            for (int c = 0; c < d; ++c) acc += ((N - 1 - l) % 2 == 0 ? g0[J * d + c] : g1[J * d + c]) * dl[c];
+                        }
                         const Real v = cb[LY::top_off(l) + J] + inv * acc;
                         if ((N - 1 - l) % 2 == 0) g1[J] = v;
                         else g0[J] = v;
@@ -387,19 +402,53 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
             ab[m - 1] = gcur;
         }
         // ---- δ̄_s = segmented sum of the lanes' partials
-        __syncwarp();
+        if constexpr (SLOTS == 1 && d <= 5) {
+            // one item per warp: transposed butterfly over 32 lanes (idle lanes hold
+            // zeros). After the xor-16/8/4 rounds lane l keeps component (l >> 2) & 7
+            // of its half-sums; xor-2/1 finish it.
+            Real v8[8];
 #pragma unroll
-        for (int c = 0; c < d; ++c) {
-            Real v = gd[c];
+            for (int c = 0; c < 8; ++c) {
+                Real v = Real(0);
+                if (c < d) {
+                    v = gd[c];
 #pragma unroll
-            for (int k = 1; k <= Q; ++k) v += dg[k] == c ? gk[k] : Real(0);
-            rd[lane][c] = v;
-        }
-        __syncwarp();
-        if (on && p < d) {
-            Real sum = Real(0);
-            for (int q = 0; q < P; ++q) sum += rd[slot * P + q][p];
-            dbar[(b * M + s) * d + p] = sum;
+                    for (int k = 1; k <= Q; ++k) v += dg[k] == c ? gk[k] : Real(0);
+                }
+                v8[c] = v;
+            }
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+            Real w4[4], w2[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const Real mine = b4 ? v8[4 + i] : v8[i], other = b4 ? v8[i] : v8[4 + i];
+                w4[i] = mine + __shfl_xor_sync(0xffffffffu, other, 16);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const Real mine = b3 ? w4[2 + i] : w4[i], other = b3 ? w4[i] : w4[2 + i];
+                w2[i] = mine + __shfl_xor_sync(0xffffffffu, other, 8);
+            }
+            Real w = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w2[0] : w2[1], 4);
+            w += __shfl_xor_sync(0xffffffffu, w, 2);
+            w += __shfl_xor_sync(0xffffffffu, w, 1);
+            const int c = (lane >> 2) & 7;
+            if ((lane & 3) == 0 && c < d && item < items && s >= s_lo) dbar[(b * M + s) * d + c] = w;
+        } else {
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < d; ++c) {
+                Real v = gd[c];
+#pragma unroll
+                for (int k = 1; k <= Q; ++k) v += dg[k] == c ? gk[k] : Real(0);
+                rd[lane][c] = v;
+            }
+            __syncwarp();
+            if (on && p < d) {
+                Real sum = Real(0);
+                for (int q = 0; q < P; ++q) sum += rd[slot * P + q][p];
+                dbar[(b * M + s) * d + p] = sum;
+            }
         }
 #pragma unroll
         for (int i = 0; i < S; ++i) cb[i] = on ? ab[i] : cb[i];
