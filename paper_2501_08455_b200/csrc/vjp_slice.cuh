@@ -465,74 +465,87 @@ struct ChunkPasses {
     // terms in the adjoint sum of a level-n entry: Σ_{k=1}^{N-n} d^k
     __host__ __device__ static constexpr int terms(int n) { return n >= N ? 0 : level_off(d, N - n); }
     __host__ __device__ static constexpr bool wide(int n) { return terms(n) >= 64; }
+    // Entry loops have compile-time trip counts (NT threads per CTA), so each
+    // thread's index math is loop-invariant across the chunk steps.
+    static constexpr int NT = 256, NW = NT / 32;
     // nxt = cur pulled back through right multiplication by sig (the adjoint of
     // cur ↦ cur ⊠ sig): entry I of level n sums Σ_k Σ_J cur[n+k][I·d^k + J]·sig[k][J].
     // Wide levels: one warp per entry, lanes split J, butterfly sum (fixed order).
     template <int n>
     __device__ __forceinline__ static void adjoint_wide(const Real* __restrict__ cur, const Real* __restrict__ sig,
-                                                        Real* __restrict__ nxt, Real* __restrict__ grow) {
+                                                        Real* __restrict__ nxt) {
         if constexpr (n <= N) {
             if constexpr (wide(n)) {
-                const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-                for (int I = w; I < ipow(d, n); I += nw) {
-                    Real acc = Real(0);
+                const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
-                    for (int k = 1; n + k <= N; ++k) {
-                        const Real* cr = cur + off(n + k - 1) + I * ipow(d, k);
-                        const Real* er = sig + off(k - 1);
-                        for (int J = lane; J < ipow(d, k); J += 32) acc = fma(cr[J], er[J], acc);
-                    }
+                for (int it = 0; it < (ipow(d, n) + NW - 1) / NW; ++it) {
+                    const int I = w + it * NW;
+                    if (I < ipow(d, n)) {
+                        Real acc = Real(0);
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                    if (lane == 0) {
-                        acc += cur[off(n - 1) + I];
-                        nxt[off(n - 1) + I] = acc;
-                        grow[off(n - 1) + I] = acc;
+                        for (int k = 1; n + k <= N; ++k) {
+                            const Real* cr = cur + off(n + k - 1) + I * ipow(d, k);
+                            const Real* er = sig + off(k - 1);
+#pragma unroll
+                            for (int jt = 0; jt < (ipow(d, k) + 31) / 32; ++jt) {
+                                const int J = lane + 32 * jt;
+                                if (J < ipow(d, k)) acc = fma(cr[J], er[J], acc);
+                            }
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                        if (lane == 0) nxt[off(n - 1) + I] = acc + cur[off(n - 1) + I];
                     }
                 }
             }
-            adjoint_wide<n + 1>(cur, sig, nxt, grow);
+            adjoint_wide<n + 1>(cur, sig, nxt);
         }
     }
     // narrow levels: one thread per entry
     template <int n>
     __device__ __forceinline__ static void adjoint_narrow(const Real* __restrict__ cur, const Real* __restrict__ sig,
-                                                          Real* __restrict__ nxt, Real* __restrict__ grow) {
+                                                          Real* __restrict__ nxt) {
         if constexpr (n <= N) {
             if constexpr (!wide(n)) {
-                // reversed thread order: the first warps carry the wide entries
-                for (int I = blockDim.x - 1 - threadIdx.x; I < ipow(d, n); I += blockDim.x) {
-                    Real acc = cur[off(n - 1) + I];
 #pragma unroll
-                    for (int k = 1; n + k <= N; ++k) {
-                        const Real* cr = cur + off(n + k - 1) + I * ipow(d, k);
-                        const Real* er = sig + off(k - 1);
+                for (int it = 0; it < (ipow(d, n) + NT - 1) / NT; ++it) {
+                    // reversed thread order: the first warps carry the wide entries
+                    const int I = NT - 1 - (int)threadIdx.x + it * NT;
+                    if (I < ipow(d, n)) {
+                        Real acc = cur[off(n - 1) + I];
 #pragma unroll
-                        for (int J = 0; J < ipow(d, k); ++J) acc = fma(cr[J], er[J], acc);
+                        for (int k = 1; n + k <= N; ++k) {
+                            const Real* cr = cur + off(n + k - 1) + I * ipow(d, k);
+                            const Real* er = sig + off(k - 1);
+#pragma unroll
+                            for (int J = 0; J < ipow(d, k); ++J) acc = fma(cr[J], er[J], acc);
+                        }
+                        nxt[off(n - 1) + I] = acc;
                     }
-                    nxt[off(n - 1) + I] = acc;
-                    grow[off(n - 1) + I] = acc;
                 }
             }
-            adjoint_narrow<n + 1>(cur, sig, nxt, grow);
+            adjoint_narrow<n + 1>(cur, sig, nxt);
         }
     }
     // nxt = cur ⊠ sig (Chen product)
     template <int n>
     __device__ __forceinline__ static void product(const Real* __restrict__ cur, const Real* __restrict__ sig,
-                                                   Real* __restrict__ nxt, Real* __restrict__ grow) {
+                                                   Real* __restrict__ nxt) {
         if constexpr (n <= N) {
-            for (int I = threadIdx.x; I < ipow(d, n); I += blockDim.x) {
-                Real v = cur[off(n - 1) + I] + sig[off(n - 1) + I];
 #pragma unroll
-                for (int a = 1; a < n; ++a) {
-                    const int tail = ipow(d, n - a);
-                    v = fma(cur[off(a - 1) + I / tail], sig[off(n - a - 1) + I % tail], v);
+            for (int it = 0; it < (ipow(d, n) + NT - 1) / NT; ++it) {
+                const int I = (int)threadIdx.x + it * NT;
+                if (I < ipow(d, n)) {
+                    Real v = cur[off(n - 1) + I] + sig[off(n - 1) + I];
+#pragma unroll
+                    for (int a = 1; a < n; ++a) {
+                        const int tail = ipow(d, n - a);
+                        v = fma(cur[off(a - 1) + I / tail], sig[off(n - a - 1) + I % tail], v);
+                    }
+                    nxt[off(n - 1) + I] = v;
                 }
-                nxt[off(n - 1) + I] = v;
-                grow[off(n - 1) + I] = v;
             }
-            product<n + 1>(cur, sig, nxt, grow);
+            product<n + 1>(cur, sig, nxt);
         }
     }
 };
@@ -545,7 +558,7 @@ struct ChunkPasses {
 // signatures are staged in shared memory up front ((U + 4) D values);
 // otherwise each step stages its two rows ((4 + 2) D values).
 template <typename Real, int d, int N>
-__global__ void __launch_bounds__(256) vjp_chunk_passes_kernel(const Real* __restrict__ C, const Real* __restrict__ cot,
+__global__ void __launch_bounds__(ChunkPasses<Real, d, N>::NT) vjp_chunk_passes_kernel(const Real* __restrict__ C, const Real* __restrict__ cot,
                                                                int U, int resident, Real* __restrict__ cbars,
                                                                Real* __restrict__ ends) {
     using CP = ChunkPasses<Real, d, N>;
@@ -591,9 +604,9 @@ __global__ void __launch_bounds__(256) vjp_chunk_passes_kernel(const Real* __res
             sB = sigs + D;
         }
         __syncthreads();
-        if (jb >= 1) CP::template adjoint_wide<1>(curB, sB, nxtB, cbars + (b * U + jb - 1) * D);
-        CP::template product<1>(curF, sF, nxtF, ends + (b * U + t) * D);
-        if (jb >= 1) CP::template adjoint_narrow<1>(curB, sB, nxtB, cbars + (b * U + jb - 1) * D);
+        if (jb >= 1) CP::template adjoint_wide<1>(curB, sB, nxtB);
+        CP::template product<1>(curF, sF, nxtF);
+        if (jb >= 1) CP::template adjoint_narrow<1>(curB, sB, nxtB);
         __syncthreads();
         Real* x = curF;
         curF = nxtF;
@@ -601,6 +614,13 @@ __global__ void __launch_bounds__(256) vjp_chunk_passes_kernel(const Real* __res
         x = curB;
         curB = nxtB;
         nxtB = x;
+        // rows out (coalesced; the next step writes the other buffers)
+        Real* ef = ends + (b * U + t) * D;
+        Real* cf = cbars + (b * U + (jb >= 1 ? jb - 1 : 0)) * D;
+        for (int i = tid; i < D; i += nth) {
+            ef[i] = curF[i];
+            if (jb >= 1) cf[i] = curB[i];
+        }
     }
 }
 
