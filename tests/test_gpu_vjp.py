@@ -109,3 +109,14 @@ def test_vjp_f32_long_chunks(sk, chunks):
     ref = O.ref_vjp(X.astype(np.float32).astype(np.float64), 4, cot.astype(np.float32).astype(np.float64))
     print("chunks", st.chunks, "steps per chunk", st.fold_steps, "rel", rel(got, ref))
     assert rel(got, ref) <= 1e-4, rel(got, ref)
+
+
+def test_vjp_many_chunks_streamed_passes(sk):
+    # (U + 4) D fp64 values exceed the chunk pass's shared-memory budget: the
+    # chunk signatures are streamed one row per step instead of staged up front
+    X = walk(2, 600, 5, seed=23)
+    cot = np.random.default_rng(24).standard_normal((2, sk.sig_dim(5, 4)))
+    st = sk.KernelStats()
+    got = sk.signature_vjp(X, 4, cot, chunks=30, stats=st)
+    assert st.chunks == 30
+    assert rel(got, O.ref_vjp(X, 4, cot)) <= 1e-10
