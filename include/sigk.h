@@ -138,7 +138,8 @@ int sigk_signature_stream_f64(const double* X, size_t B, size_t L, int d, int N,
 
 /* Reverse mode: grad (B, L, d) = d<cotangent, Sig(X)>/dX for cotangent (B, D).
  * flags: SIGK_X_ON_DEVICE means X, cotangent and grad are all device buffers
- * (asynchronous on `stream`); otherwise all three are host buffers. */
+ * (asynchronous on `stream`); otherwise all three are host buffers. grad must
+ * not overlap X or cotangent (it is written while X is still being read). */
 int sigk_signature_vjp_f32(const float* X, size_t B, size_t L, int d, int N, const float* cotangent, float* grad,
                            unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats);
 int sigk_signature_vjp_f64(const double* X, size_t B, size_t L, int d, int N, const double* cotangent, double* grad,

@@ -1086,7 +1086,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             const size_t psm = resident ? rsm : 6 * D * sizeof(Real);
             if (psm > 48 * 1024)
                 cudaFuncSetAttribute(sl.passes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::min<size_t>(psm, 227 * 1024));
-            sl.passes<<<(unsigned)B, 256, psm, s>>>(C, cot, U, resident, cb, ends);
+            sl.passes<<<(unsigned)B, 256, psm, s>>>(C, cot, U, resident, cb, ends, L, CL, grad);
             launches += 1;
         } else {
             if (bsm > 48 * 1024)
@@ -1095,8 +1095,8 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             launches += 1;
         }
     }
-    Real* dbar = nullptr;
-    if (M > 0 && (e = alloc(reinterpret_cast<void**>(&dbar), sizeof(Real) * B * M * d)) != cudaSuccess) {
+    Real* dbar = nullptr;  // element-parallel kernel: δ̄ rows, then vjp_grad_kernel
+    if (M > 0 && !sl.fn && (e = alloc(reinterpret_cast<void**>(&dbar), sizeof(Real) * B * M * d)) != cudaSuccess) {
         release();
         return cuda_fail(e, "vjp allocation");
     }
@@ -1126,7 +1126,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, sl.fn, X, L, items, U, CL, static_cast<const Real*>(ends), cbars, dbar);
+        e = cudaLaunchKernelEx(&cfg, sl.fn, X, L, items, U, CL, static_cast<const Real*>(ends), cbars, grad);
         if (e != cudaSuccess) {
             release();
             return cuda_fail(e, "vjp slice launch");
@@ -1154,10 +1154,12 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         }
         launches += 1;
     }
-    const int64_t ng = B * L * d;
-    vjp_grad_kernel<Real><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((ng + 255) / 256, sms * 16)), 256, 0, s>>>(
-        dbar, B, L, d, grad);
-    launches += 1;
+    if (!(M > 0 && sl.fn)) {  // the slice walk writes ∂/∂X itself
+        const int64_t ng = B * L * d;
+        vjp_grad_kernel<Real><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((ng + 255) / 256, sms * 16)), 256, 0, s>>>(
+            dbar, B, L, d, grad);
+        launches += 1;
+    }
     e = cudaPeekAtLastError();
     release();
     if (e != cudaSuccess) return cuda_fail(e, "vjp launch");
@@ -1177,6 +1179,15 @@ static int vjp_impl(const Real* X, size_t B, size_t L, int d, int N, const Real*
     int rc = validate(X, B, L, d, N, grad);
     if (rc != SIGK_OK) return rc;
     if (cot == nullptr) return fail(SIGK_EDOMAIN, "signature_vjp: cotangent pointer is null");
+    {
+        size_t D = 0;
+        sigk_sig_dim(d, N, &D);
+        const auto a = reinterpret_cast<uintptr_t>(grad), ae = a + sizeof(Real) * B * L * d;
+        const auto x = reinterpret_cast<uintptr_t>(X), xe = x + sizeof(Real) * B * L * d;
+        const auto c = reinterpret_cast<uintptr_t>(cot), ce = c + sizeof(Real) * B * D;
+        if ((a < xe && x < ae) || (a < ce && c < ae))
+            return fail(SIGK_EDOMAIN, "signature_vjp: grad must not overlap the paths or the cotangent");
+    }
     if (N > kGenericMaxDepth) return fail(SIGK_ERESOURCE, "signature_vjp: depth above 16 is not supported");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     size_t D = 0;

@@ -234,7 +234,7 @@ struct VjpSlice {
     void (*fn)(const Real*, int64_t, int64_t, int, int64_t, const Real*, const Real*, Real*) = nullptr;
     int slots = 0;  // (path, chunk) items per warp
     // compile-time boundary + ends pass (vjp_chunk_passes_kernel); null: the runtime kernels
-    void (*passes)(const Real*, const Real*, int, int, Real*, Real*) = nullptr;
+    void (*passes)(const Real*, const Real*, int, int, Real*, Real*, int64_t, int64_t, Real*) = nullptr;
 };
 VjpSlice<float> vjp_slice_for_f32(int d, int N);
 VjpSlice<double> vjp_slice_for_f64(int d, int N);

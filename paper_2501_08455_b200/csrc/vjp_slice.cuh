@@ -231,7 +231,7 @@ struct SliceGather {
 template <typename Real, int d, int N, int Q>
 __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__ X, int64_t L, int64_t items,
                                                         int U, int64_t CL, const Real* __restrict__ ends,
-                                                        const Real* __restrict__ cbars, Real* __restrict__ dbar) {
+                                                        const Real* __restrict__ cbars, Real* __restrict__ grad) {
     using LY = SliceLayout<d, N, Q>;
     constexpr int P = LY::P, SLOTS = LY::SLOTS, S = LY::S, NLOW = LY::NLOW, VS = LY::VS, GMAX = LY::GMAX;
     constexpr int D = level_off(d, N);
@@ -289,6 +289,13 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
         phi[k] = any ? xb[s_hi * d + dg[k]] : Real(0);
         plo[k] = any ? xb[(s_hi - 1) * d + dg[k]] : Real(0);
     }
+    // ∂/∂X_t = δ̄_{t-1} - δ̄_t, written as the walk goes: interior points of the
+    // chunk and the path's end points directly, a point shared with a
+    // neighbouring chunk by an atomic add onto the zero the chunk pass left
+    // there (two terms from two chunks: the sum is order independent)
+    const bool first_chunk = j == 0, last_chunk = j == U - 1;
+    Real* gb = grad + b * L * d;
+    Real prev = Real(0);  // δ̄_{s+1} of this lane's component
     for (int64_t st = 0; st < CL; ++st) {
         const int64_t s = s_hi - 1 - st;
         const bool on = valid && s >= s_lo;
@@ -433,7 +440,16 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
             w += __shfl_xor_sync(0xffffffffu, w, 2);
             w += __shfl_xor_sync(0xffffffffu, w, 1);
             const int c = (lane >> 2) & 7;
-            if ((lane & 3) == 0 && c < d && item < items && s >= s_lo) dbar[(b * M + s) * d + c] = w;
+            if ((lane & 3) == 0 && c < d && item < items && s >= s_lo) {
+                if (st > 0) gb[(s + 1) * d + c] = w - prev;
+                else if (last_chunk) gb[(s + 1) * d + c] = w;
+                else atomicAdd(gb + (s + 1) * d + c, w);
+                if (s == s_lo) {
+                    if (first_chunk) gb[s * d + c] = -w;
+                    else atomicAdd(gb + s * d + c, -w);
+                }
+                prev = w;
+            }
         } else {
             __syncwarp();
 #pragma unroll
@@ -447,7 +463,14 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
             if (on && p < d) {
                 Real sum = Real(0);
                 for (int q = 0; q < P; ++q) sum += rd[slot * P + q][p];
-                dbar[(b * M + s) * d + p] = sum;
+                if (st > 0) gb[(s + 1) * d + p] = sum - prev;
+                else if (last_chunk) gb[(s + 1) * d + p] = sum;
+                else atomicAdd(gb + (s + 1) * d + p, sum);
+                if (s == s_lo) {
+                    if (first_chunk) gb[s * d + p] = -sum;
+                    else atomicAdd(gb + s * d + p, -sum);
+                }
+                prev = sum;
             }
         }
 #pragma unroll
@@ -560,7 +583,8 @@ struct ChunkPasses {
 template <typename Real, int d, int N>
 __global__ void __launch_bounds__(ChunkPasses<Real, d, N>::NT) vjp_chunk_passes_kernel(const Real* __restrict__ C, const Real* __restrict__ cot,
                                                                int U, int resident, Real* __restrict__ cbars,
-                                                               Real* __restrict__ ends) {
+                                                               Real* __restrict__ ends, int64_t L, int64_t CL,
+                                                               Real* __restrict__ grad) {
     using CP = ChunkPasses<Real, d, N>;
     constexpr int D = CP::D;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -574,6 +598,8 @@ __global__ void __launch_bounds__(ChunkPasses<Real, d, N>::NT) vjp_chunk_passes_
     const Real* Cb = C + b * U * D;
     pdl_trigger();
     pdl_wait();
+    // the slice walk adds the two chunks' terms of every shared chunk point onto zeros
+    for (int i = tid; i < (U - 1) * d; i += nth) grad[(b * L + (int64_t)(i / d + 1) * CL) * d + i % d] = Real(0);
     if (resident) {  // the predecessor's rows: L2, not L1; 16-byte loads when aligned
         const size_t bytes = (size_t)U * D * sizeof(Real);
         if (bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(Cb) & 15) == 0) {

@@ -56,6 +56,20 @@ def test_domain_errors_before_any_device_work(sk):
         sk.signature_parallel(np.zeros((4, 32, 3)), 3, memory_cap=1000)
 
 
+def test_vjp_refuses_aliased_gradient(sk):
+    # grad is written while the paths are still read: overlap is a domain error, raised before device work
+    import ctypes as C
+
+    X = np.zeros((2, 5, 3), np.float32)
+    cot = np.zeros((2, 39), np.float32)
+    lib = sk.lib()
+    fp = C.POINTER(C.c_float)
+    rc = lib.sigk_signature_vjp_f32(X.ctypes.data_as(fp), C.c_size_t(2), C.c_size_t(5), 3, 3, cot.ctypes.data_as(fp),
+                                    X.ctypes.data_as(fp), C.c_uint(0), None, None, None)
+    assert rc == 1
+    assert b"overlap" in lib.sigk_last_error()
+
+
 def test_no_silent_cpu_fallback_without_gpu(sk):
     import torch
 
