@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
     for (int k = 1; k < Q; ++k) low[k - 1] = level_off(d, k - 1) + p / ipow(d, Q - k);
 #pragma unroll
     for (int n = Q; n <= N; ++n) lvl[n - Q] = level_off(d, n - 1) + p * ipow(d, n - Q);
-    Real cb[S], a[S], an[S];
+    Real cb[S], an[S];
     const Real* crow = cbars + it * D;
     auto gather = [&](const Real* __restrict__ row, bool ok, Real(&dst)[S]) {
 #pragma unroll
@@ -327,8 +327,10 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
 #pragma unroll
             for (int k = 1; k <= Q; ++k) ndp[k] = -dp[k];
             SliceFold<Real, d, N, Q>::template levels<N>(an, ndl, ndp);
+            if (s == 0) {  // S_0: the identity, exactly (a branch, not S selects per step)
 #pragma unroll
-            for (int i = 0; i < S; ++i) a[i] = s == 0 ? Real(0) : an[i];  // S_0: the identity, exactly
+                for (int i = 0; i < S; ++i) an[i] = Real(0);
+            }
         }
         Real gd[d], gk[Q + 1];
 #pragma unroll
@@ -336,7 +338,7 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
 #pragma unroll
         for (int k = 0; k <= Q; ++k) gk[k] = Real(0);
         // ---- δ̄: reverse through each level's Horner chain (owned outputs only)
-        SliceRev<Real, d, N, Q>::template levels<1>(a, cb, dl, dp, gd, gk, p);
+        SliceRev<Real, d, N, Q>::template levels<1>(an, cb, dl, dp, gd, gk, p);
         // ---- Ā = C̄ pulled back through ⊠ exp(δ)
         Real ab[S];
 #pragma unroll
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
                     gcur = sc(cb, l) + (Real(1) / Real(l - m + 1)) * sum;
                 }
             }
-            ab[m - 1] = gcur;
+            ab[m - 1] = lane_on ? gcur : Real(0);  // idle lanes read slot 0's sums: keep them at zero
         }
         // ---- δ̄_s = segmented sum of the lanes' partials
         if constexpr (SLOTS == 1 && d <= 5) {
@@ -473,8 +475,11 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
                 prev = sum;
             }
         }
+        // steps past a short chunk's start run with δ = 0, where the pull-back is
+        // the identity (Ā == C̄ exactly), so no per-step select is needed (idle
+        // lanes stay at zero: their only nonzero inputs, the low-level sums, are masked)
 #pragma unroll
-        for (int i = 0; i < S; ++i) cb[i] = on ? ab[i] : cb[i];
+        for (int i = 0; i < S; ++i) cb[i] = ab[i];
     }
 }
 
