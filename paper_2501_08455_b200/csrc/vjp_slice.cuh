@@ -248,6 +248,12 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
     int dg[Q + 1];  // digits p_1..p_Q
 #pragma unroll
     for (int k = 1; k <= Q; ++k) dg[k] = (p / ipow(d, Q - k)) % d;
+    // 1 where digit p_k is channel c: folds the lane's δ[p_k] partials into δ̄ by FMA
+    Real dmask[Q + 1][d];
+#pragma unroll
+    for (int k = 1; k <= Q; ++k)
+#pragma unroll
+        for (int c = 0; c < d; ++c) dmask[k][c] = dg[k] == c ? Real(1) : Real(0);
     Real (&rd)[32][d + 1] = red[warp];
 
     // the lane's slice inside a signature row: low scalars at level k (k < Q),
@@ -422,7 +428,7 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
                 if (c < d) {
                     v = gd[c];
 #pragma unroll
-                    for (int k = 1; k <= Q; ++k) v += dg[k] == c ? gk[k] : Real(0);
+                    for (int k = 1; k <= Q; ++k) v = fma(dmask[k][c], gk[k], v);
                 }
                 v8[c] = v;
             }
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
             for (int c = 0; c < d; ++c) {
                 Real v = gd[c];
 #pragma unroll
-                for (int k = 1; k <= Q; ++k) v += dg[k] == c ? gk[k] : Real(0);
+                for (int k = 1; k <= Q; ++k) v = fma(dmask[k][c], gk[k], v);
                 rd[lane][c] = v;
             }
             __syncwarp();
