@@ -1034,6 +1034,22 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         // latency-bound per item: long paths want more, shorter items)
         const int64_t want = std::max<int64_t>(((int64_t)sms * 8 + B - 1) / B, M / 250);
         U = (int)std::max<int64_t>(1, std::min<int64_t>(want, M / 16));
+        if (sl.fn) {
+            // the slice walk is issue-bound per SM: its time follows the CTAs the
+            // busiest SM runs (4 warps each) times the steps per chunk, so pick U
+            // in [want/2, 2 want] minimising that (ties: fewer chunks, cheaper
+            // chunk passes). C2: U = 8 (2 CTAs per SM x 125 steps) beats 10 (3 x 100).
+            int64_t best = -1;
+            const int64_t lo = std::max<int64_t>(2, want / 2), hi = std::min<int64_t>(2 * want, M / 16);
+            for (int64_t u = lo; u <= hi; ++u) {
+                const int64_t cl = (M + u - 1) / u, ctas = (B * u + 4 * sl.slots - 1) / (4 * sl.slots);
+                const int64_t cost = (ctas + sms - 1) / sms * cl;
+                if (best < 0 || cost < best) {
+                    best = cost;
+                    U = (int)u;
+                }
+            }
+        }
         if (tun && tun->chunks > 1) U = (int)std::min<int64_t>(tun->chunks, M);
     }
     const int64_t CL = M > 0 ? (M + U - 1) / U : 1;
