@@ -1038,7 +1038,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             // the slice walk is issue-bound per SM: its time follows the CTAs the
             // busiest SM runs (4 warps each) times the steps per chunk, so pick U
             // in [want/2, 2 want] minimising that (ties: fewer chunks, cheaper
-            // chunk passes). C2: U = 8 (2 CTAs per SM x 125 steps) beats 10 (3 x 100).
+            // chunk passes). C2: U = 9 (2 CTAs per SM x 111 steps) beats 10 (3 x 100).
             int64_t best = -1;
             const int64_t lo = std::max<int64_t>(2, want / 2), hi = std::min<int64_t>(2 * want, M / 16);
             for (int64_t u = lo; u <= hi; ++u) {
