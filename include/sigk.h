@@ -12,6 +12,11 @@
  *   sigk_signature_f32    ← detail::sequential_forward<float>
  *                           include/sigkit/detail/sig_core.hpp:120-147 (the raw-pointer core the
  *                           reference bench instantiates for float, src/bench.cpp:29-56)
+ *   sigk_signature_parallel_f32/_f64
+ *                         ← sigkit::signature_parallel (KernelKind::Parallel)  include/sigkit/kernels.hpp:103-108,
+ *                           src/kernels.cpp:124-148, detail::parallel_forward sig_core.hpp:175-298 (the paper's
+ *                           per-degree cumulative-sum formulation, run as N GPU scan passes; with
+ *                           SIGK_PREFIX_ROWS also signature_stream over the parallel kernel, kernels.cpp:183-197)
  *   sigk_signature_stream_f32/_f64
  *                         ← sigkit::signature_stream  include/sigkit/kernels.hpp:110-114,
  *                           src/kernels.cpp:156-198 (every prefix signature, (B, L-1, D);
@@ -72,11 +77,20 @@ extern "C" {
  * streams, so the H2D of call i+1 overlaps the kernels and D2H of call i
  * (throughput bound by PCIe, not by the sum of the three). */
 #define SIGK_ASYNC_HOST 4u
+/* sigk_signature_parallel_* only: `out` is (B, L-1, D), every prefix
+ * signature (the reference's PrefixSignatureBatch); L < 2 is a DomainError. */
+#define SIGK_PREFIX_ROWS 8u
 
-/* Structural counters (the reference KernelStats, kernels.hpp:86-91, plus
- * the GPU decomposition). fold_steps = increments folded by each (path,
- * chunk) unit = ceil((L-1)/(segments*chunks)); scan_passes = combine
- * rounds = ceil(log2(chunks)) (+ ceil(log2(segments)) when segmented). */
+/* Structural counters, all taken from the launches the call actually made.
+ * Chunked-fold families (PATH/FLAT/PAIR/PFLAT/GENERIC): fold_steps = the
+ * longest run of increments one (path, chunk) unit folds sequentially =
+ * ceil((L-1)/(segments*chunks)); scan_passes = rounds of the cross-chunk
+ * combine = ceil(log2(chunks)) (+ ceil(log2(segments)) when segmented);
+ * path_steps = Chen fold steps applied per path, summed over the path's
+ * units from the launch geometry (= L-1: the reference's fold_steps,
+ * kernels.cpp:117-120). SCAN family (sigk_signature_parallel_*): fold_steps
+ * = 0 and scan_passes = the degree passes launched (= depth: the reference's
+ * scan_passes, kernels.cpp:143-146), path_steps = 0. */
 typedef struct sigk_stats {
     int64_t fold_steps;
     int64_t scan_passes;
@@ -86,6 +100,7 @@ typedef struct sigk_stats {
     int32_t launches;     /* kernels launched by the call */
     int32_t segments;     /* G: CTAs per path (pair family; 1 otherwise) */
     int32_t family;       /* SIGK_FAMILY_* of the fold kernel */
+    int64_t path_steps;   /* fold steps applied per path (see above) */
 } sigk_stats;
 
 /* fold-kernel families (sigk_stats.family, sigk_tuning.family) */
@@ -95,6 +110,7 @@ typedef struct sigk_stats {
 #define SIGK_FAMILY_PAIR 3    /* packed FP32x2 (FFMA2) chunk pairs, segment CTAs (fp32) */
 #define SIGK_FAMILY_GENERIC 4 /* shape-generic correctness kernel */
 #define SIGK_FAMILY_PFLAT 5   /* packed FP32x2 along the last index (even d), whole paths, no chunking (fp32) */
+#define SIGK_FAMILY_SCAN 6    /* the paper's per-degree cumulative-sum formulation (KernelKind::Parallel) */
 
 /* Optional tuning overrides (NULL or zero fields = automatic). */
 typedef struct sigk_tuning {
@@ -135,6 +151,18 @@ int sigk_signature_stream_f32(const float* X, size_t B, size_t L, int d, int N, 
                               void* stream, const sigk_tuning* tuning, sigk_stats* stats);
 int sigk_signature_stream_f64(const double* X, size_t B, size_t L, int d, int N, double* out, unsigned flags,
                               void* stream, const sigk_tuning* tuning, sigk_stats* stats);
+
+/* The paper's parallel formulation (KernelKind::Parallel): N per-degree
+ * passes, each a GPU cumulative-sum scan over the sequence of per-position
+ * contributions, materialising every per-position level (B·(L-1)·D scalars of
+ * device workspace, stream-ordered). SIGK_ERESOURCE with the reference's
+ * message when B·L·d^N > memory_cap (sig_core.hpp:161-173; the reference
+ * default is 2^31, kDefaultParallelMemoryCap) or depth > 64. Flags as for
+ * sigk_signature_* plus SIGK_PREFIX_ROWS; SIGK_ASYNC_HOST is not supported. */
+int sigk_signature_parallel_f32(const float* X, size_t B, size_t L, int d, int N, float* out, size_t memory_cap,
+                                unsigned flags, void* stream, sigk_stats* stats);
+int sigk_signature_parallel_f64(const double* X, size_t B, size_t L, int d, int N, double* out, size_t memory_cap,
+                                unsigned flags, void* stream, sigk_stats* stats);
 
 /* Reverse mode: grad (B, L, d) = d<cotangent, Sig(X)>/dX for cotangent (B, D).
  * flags: SIGK_X_ON_DEVICE means X, cotangent and grad are all device buffers

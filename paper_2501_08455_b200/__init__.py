@@ -27,7 +27,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SIGK_LIB_PATH") or os.path.join(_HERE, "libsigk.so")
 
 SIGK_OK, SIGK_EDOMAIN, SIGK_ERESOURCE, SIGK_EDEVICE, SIGK_ETRAINING = 0, 1, 2, 3, 4
-SIGK_X_ON_DEVICE, SIGK_OUT_ON_DEVICE, SIGK_ASYNC_HOST = 1, 2, 4
+SIGK_X_ON_DEVICE, SIGK_OUT_ON_DEVICE, SIGK_ASYNC_HOST, SIGK_PREFIX_ROWS = 1, 2, 4, 8
+DEFAULT_PARALLEL_MEMORY_CAP = 1 << 31  # reference kDefaultParallelMemoryCap (kernels.hpp:93)
 
 
 class DomainError(ValueError):
@@ -54,7 +55,7 @@ class DeviceError(RuntimeError):
 class _Stats(C.Structure):
     _fields_ = [("fold_steps", C.c_int64), ("scan_passes", C.c_int64), ("chunks", C.c_int32),
                 ("prefix_len", C.c_int32), ("threads_per_unit", C.c_int32), ("launches", C.c_int32),
-                ("segments", C.c_int32), ("family", C.c_int32)]
+                ("segments", C.c_int32), ("family", C.c_int32), ("path_steps", C.c_int64)]
 
 
 class _Tuning(C.Structure):
@@ -66,7 +67,12 @@ class _Tuning(C.Structure):
 
 @dataclass
 class KernelStats:
-    """Reference KernelStats (kernels.hpp:86-91) plus the GPU decomposition."""
+    """The C ABI's sigk_stats (include/sigk.h), all taken from the launches the
+    call made. Reference KernelStats meaning (kernels.hpp:86-91): the chunked
+    fold reports ``path_steps`` = fold steps applied per path (= L-1) and
+    ``fold_steps`` = steps per chunk unit, ``scan_passes`` = combine rounds; the
+    parallel formulation (family FAMILY_SCAN) reports ``scan_passes`` = degree
+    passes launched (= depth) and ``fold_steps`` = 0."""
     fold_steps: int = 0
     scan_passes: int = 0
     chunks: int = 0
@@ -75,11 +81,12 @@ class KernelStats:
     launches: int = 0
     segments: int = 0
     family: int = 0
+    path_steps: int = 0
 
 
 # fold-kernel families (include/sigk.h SIGK_FAMILY_*)
-FAMILY_AUTO, FAMILY_PATH, FAMILY_FLAT, FAMILY_PAIR, FAMILY_GENERIC, FAMILY_PFLAT = 0, 1, 2, 3, 4, 5
-FAMILY_NAMES = {0: "auto", 1: "path", 2: "flat", 3: "pair", 4: "generic", 5: "pflat"}
+FAMILY_AUTO, FAMILY_PATH, FAMILY_FLAT, FAMILY_PAIR, FAMILY_GENERIC, FAMILY_PFLAT, FAMILY_SCAN = 0, 1, 2, 3, 4, 5, 6
+FAMILY_NAMES = {0: "auto", 1: "path", 2: "flat", 3: "pair", 4: "generic", 5: "pflat", 6: "scan"}
 
 
 class KernelKind(enum.Enum):
@@ -101,14 +108,16 @@ def kernel_from_name(name: str) -> KernelKind:
 
 @dataclass
 class ExecutionCaps:
-    """Reference kernels.hpp:76-84; kept for source compatibility."""
-    accelerated: bool = True
+    """Reference kernels.hpp:76-84 (same defaults): Auto resolves to Parallel
+    only when ``accelerated`` and ``seq_len >= parallel_min_len``."""
+    accelerated: bool = False
     parallel_min_len: int = 64
 
     @staticmethod
     def detect() -> "ExecutionCaps":
+        """SIGKIT_ACCELERATED set, non-empty and not "0" (kernels.cpp:64-69)."""
         env = os.environ.get("SIGKIT_ACCELERATED")
-        return ExecutionCaps(accelerated=env is None or env != "0")
+        return ExecutionCaps(accelerated=env is not None and env not in ("", "0"))
 
 
 def select_kernel(hint: KernelKind, caps: ExecutionCaps, seq_len: int) -> KernelKind:
@@ -136,6 +145,8 @@ def lib():
         for n in ("sigk_signature_stream_f32", "sigk_signature_stream_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, C.c_uint, vp, C.POINTER(_Tuning),
                                       C.POINTER(_Stats)]
+        for n in ("sigk_signature_parallel_f32", "sigk_signature_parallel_f64"):
+            getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, sz, C.c_uint, vp, C.POINTER(_Stats)]
         for n in ("sigk_signature_vjp_f32", "sigk_signature_vjp_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, vp, C.c_uint, vp, C.POINTER(_Tuning),
                                       C.POINTER(_Stats)]
@@ -225,6 +236,49 @@ def plan(B: int, L: int, d: int, depth: int, f64: bool = False, **tuning) -> Ker
     return ks
 
 
+def _copy_stats(st: _Stats, stats: KernelStats | None):
+    if stats is not None:
+        for f, _ in _Stats._fields_:
+            setattr(stats, f, getattr(st, f))
+
+
+def _torch_dtype_ok(X):
+    import torch
+
+    if X.dtype not in (torch.float32, torch.float64):
+        raise DomainError(f"unsupported dtype {X.dtype} (float32 or float64)")
+
+
+def _host_array(paths, depth: int):
+    X = np.asarray(paths)
+    B, L, d = _validate_shape(X.shape, depth)
+    if X.dtype not in (np.float32, np.float64):
+        X = X.astype(np.float64)
+    return np.ascontiguousarray(X), B, L, d
+
+
+def _check_out(out, shape, like, *, pinned: bool = False):
+    """Validate a caller-provided ``out`` before its pointer reaches the C ABI:
+    exact shape, the input's dtype, same device (pinned host memory for the
+    asynchronous host mode), contiguous."""
+    if tuple(out.shape) != tuple(shape):
+        raise DomainError(f"out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if out.dtype != like.dtype:
+        raise DomainError(f"out has dtype {out.dtype}, expected {like.dtype}")
+    if _is_torch(out) != _is_torch(like):
+        raise DomainError("out must be the same kind of array as the paths (numpy or torch)")
+    if _is_torch(out):
+        if out.device != like.device:
+            raise DomainError(f"out is on {out.device}, paths on {like.device}")
+        if not out.is_contiguous():
+            raise DomainError("out must be contiguous")
+        if pinned and not out.is_pinned():
+            raise DomainError("async host mode needs a pinned CPU `out`")
+    elif not (out.flags["C_CONTIGUOUS"] and out.flags["WRITEABLE"]):
+        raise DomainError("out must be a writeable C-contiguous array")
+    return out
+
+
 def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_generic: bool = False,
          out=None, plan_rows: int = 0, prefix_len: int = 0, segments: int = 0, family: int = 0):
     st = _Stats()
@@ -234,47 +288,77 @@ def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_ge
         import torch
 
         B, L, d = _validate_shape(paths.shape, depth)
-        if paths.dtype not in (torch.float32, torch.float64):
-            raise DomainError(f"unsupported dtype {paths.dtype}")
+        _torch_dtype_ok(paths)
         fn = lib().sigk_signature_f32 if paths.dtype == torch.float32 else lib().sigk_signature_f64
         D = sig_dim(d, depth)
         if not paths.is_cuda:
             # page-locked host tensors: asynchronous host mode on the current CUDA
-            # stream (SIGK_ASYNC_HOST); `out` is valid once that stream is synchronised
+            # stream (SIGK_ASYNC_HOST); `out` is valid once that stream is synchronised.
+            # The input must be the caller's own contiguous pinned buffer: a temporary
+            # copy could be recycled by the pinned-memory cache while the H2D is queued.
             if not paths.is_pinned():
                 raise DomainError("torch CPU input must be pinned (async host mode); use numpy for plain host buffers")
-            X = paths if paths.is_contiguous() else paths.contiguous().pin_memory()
+            if not paths.is_contiguous():
+                raise DomainError("async host mode needs a contiguous pinned input (copies could be freed "
+                                  "before the queued host-to-device copy runs)")
+            X = paths
             if out is None:
                 out = torch.empty((B, D), dtype=X.dtype, pin_memory=True)
-            if out.is_cuda or not out.is_pinned():
+            if out.is_cuda:
                 raise DomainError("async host mode needs a pinned CPU `out`")
+            _check_out(out, (B, D), X, pinned=True)
             s = torch.cuda.current_stream().cuda_stream
             _check(fn(X.data_ptr(), B, L, d, depth, out.data_ptr(), SIGK_ASYNC_HOST, s, C.byref(tun), C.byref(st)))
-            if stats is not None:
-                for f, _ in _Stats._fields_:
-                    setattr(stats, f, getattr(st, f))
+            _copy_stats(st, stats)
             return out
         X = paths.contiguous()
-        if out is None:
-            out = torch.empty((B, D), dtype=X.dtype, device=X.device)
+        out = torch.empty((B, D), dtype=X.dtype, device=X.device) if out is None else _check_out(out, (B, D), X)
         with torch.cuda.device(X.device):
             s = torch.cuda.current_stream(X.device).cuda_stream
             _check(fn(X.data_ptr(), B, L, d, depth, out.data_ptr(), SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE,
                       s, C.byref(tun), C.byref(st)))
     else:
-        X = np.asarray(paths)
-        B, L, d = _validate_shape(X.shape, depth)
-        if X.dtype not in (np.float32, np.float64):
-            X = X.astype(np.float64)
-        X = np.ascontiguousarray(X)
+        X, B, L, d = _host_array(paths, depth)
         D = sig_dim(d, depth)
-        out = np.empty((B, D), dtype=X.dtype) if out is None else out
+        out = np.empty((B, D), dtype=X.dtype) if out is None else _check_out(out, (B, D), X)
         fn = lib().sigk_signature_f32 if X.dtype == np.float32 else lib().sigk_signature_f64
         _check(fn(X.ctypes.data, B, L, d, depth, out.ctypes.data, 0, None, C.byref(tun), C.byref(st)))
-    if stats is not None:
-        for f, _ in _Stats._fields_:
-            setattr(stats, f, getattr(st, f))
+    _copy_stats(st, stats)
     return out
+
+
+def _run_parallel(paths, depth: int, stats: KernelStats | None, memory_cap: int, prefix_rows: bool, out=None):
+    """The paper's per-degree scan formulation on the GPU (sigk_signature_parallel_*)."""
+    st = _Stats()
+    flags = SIGK_PREFIX_ROWS if prefix_rows else 0
+    if _is_torch(paths):
+        import torch
+
+        if not paths.is_cuda:
+            raise DomainError("torch input must be a CUDA tensor (use numpy for host buffers)")
+        B, L, d = _validate_shape(paths.shape, depth)
+        _torch_dtype_ok(paths)
+        X = paths.contiguous()
+        shape = (B, max(L - 1, 0), sig_dim(d, depth)) if prefix_rows else (B, sig_dim(d, depth))
+        out = torch.empty(shape, dtype=X.dtype, device=X.device) if out is None else _check_out(out, shape, X)
+        fn = lib().sigk_signature_parallel_f32 if X.dtype == torch.float32 else lib().sigk_signature_parallel_f64
+        with torch.cuda.device(X.device):
+            s = torch.cuda.current_stream(X.device).cuda_stream
+            _check(fn(X.data_ptr(), B, L, d, depth, out.data_ptr(), memory_cap,
+                      flags | SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE, s, C.byref(st)))
+    else:
+        X, B, L, d = _host_array(paths, depth)
+        shape = (B, max(L - 1, 0), sig_dim(d, depth)) if prefix_rows else (B, sig_dim(d, depth))
+        out = np.empty(shape, dtype=X.dtype) if out is None else _check_out(out, shape, X)
+        fn = lib().sigk_signature_parallel_f32 if X.dtype == np.float32 else lib().sigk_signature_parallel_f64
+        _check(fn(X.ctypes.data, B, L, d, depth, out.ctypes.data if out.size else None, memory_cap, flags, None,
+                  C.byref(st)))
+    _copy_stats(st, stats)
+    return out
+
+
+def _seq_len(paths) -> int:
+    return int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0
 
 
 def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
@@ -282,13 +366,16 @@ def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: Exe
               prefix_len: int = 0, segments: int = 0, family: int = 0):
     """Reference ``sigkit::signature`` (kernels.cpp:200-206): (B, L, d) -> (B, D).
 
-    ``kernel``/``caps`` are accepted for source compatibility; every kind runs
-    the same GPU kernels. ``chunks`` forces the sequence split (0 = planned);
+    ``kernel``/``caps`` dispatch like the reference (select_kernel,
+    kernels.cpp:150-154): Parallel runs the paper's per-degree scan
+    formulation on the GPU (``signature_parallel``), Sequential the chunked
+    Chen fold. ``chunks`` forces the sequence split of the fold (0 = planned);
     ``plan_rows`` plans the split as if the batch had that many rows (results
     are bitwise independent of batch composition at equal chunking);
     ``segments``/``family``/``prefix_len`` pin the rest of the plan (tests, tuning).
     """
-    select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
+    if select_kernel(kernel, caps or ExecutionCaps.detect(), _seq_len(paths)) == KernelKind.Parallel:
+        return signature_parallel(paths, depth, stats, out=out)
     return _run(paths, depth, stats, chunks=chunks, out=out, plan_rows=plan_rows, prefix_len=prefix_len,
                 segments=segments, family=family)
 
@@ -297,8 +384,10 @@ def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, ca
                      stats: KernelStats | None = None, *, out=None, family: int = 0, chunks: int = 0,
                      segments: int = 0):
     """Reference ``sigkit::signature_stream`` (kernels.cpp:156-198): (B, L, d) -> (B, L-1, D),
-    row (b, t) = signature of X[b, 0..t+1]. L < 2 raises DomainError."""
-    select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
+    row (b, t) = signature of X[b, 0..t+1]. L < 2 raises DomainError. The Parallel kind reads
+    every position of the per-degree scan formulation (kernels.cpp:183-197)."""
+    if select_kernel(kernel, caps or ExecutionCaps.detect(), _seq_len(paths)) == KernelKind.Parallel:
+        return _run_parallel(paths, depth, stats, DEFAULT_PARALLEL_MEMORY_CAP, True, out=out)
     st = _Stats()
     tun = _Tuning(family=family, chunks=chunks, segments=segments)
     if _is_torch(paths):
@@ -307,28 +396,22 @@ def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, ca
         if not paths.is_cuda:
             raise DomainError("torch input must be a CUDA tensor (use numpy for host buffers)")
         B, L, d = _validate_shape(paths.shape, depth)
+        _torch_dtype_ok(paths)
         X = paths.contiguous()
-        D = sig_dim(d, depth)
-        if out is None:
-            out = torch.empty((B, max(L - 1, 0), D), dtype=X.dtype, device=X.device)
+        shape = (B, max(L - 1, 0), sig_dim(d, depth))
+        out = torch.empty(shape, dtype=X.dtype, device=X.device) if out is None else _check_out(out, shape, X)
         fn = lib().sigk_signature_stream_f32 if X.dtype == torch.float32 else lib().sigk_signature_stream_f64
         with torch.cuda.device(X.device):
             s = torch.cuda.current_stream(X.device).cuda_stream
             _check(fn(X.data_ptr(), B, L, d, depth, out.data_ptr(), SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE,
                       s, C.byref(tun), C.byref(st)))
     else:
-        X = np.asarray(paths)
-        B, L, d = _validate_shape(X.shape, depth)
-        if X.dtype not in (np.float32, np.float64):
-            X = X.astype(np.float64)
-        X = np.ascontiguousarray(X)
-        D = sig_dim(d, depth)
-        out = np.empty((B, max(L - 1, 0), D), dtype=X.dtype) if out is None else out
+        X, B, L, d = _host_array(paths, depth)
+        shape = (B, max(L - 1, 0), sig_dim(d, depth))
+        out = np.empty(shape, dtype=X.dtype) if out is None else _check_out(out, shape, X)
         fn = lib().sigk_signature_stream_f32 if X.dtype == np.float32 else lib().sigk_signature_stream_f64
         _check(fn(X.ctypes.data, B, L, d, depth, out.ctypes.data, 0, None, C.byref(tun), C.byref(st)))
-    if stats is not None:
-        for f, _ in _Stats._fields_:
-            setattr(stats, f, getattr(st, f))
+    _copy_stats(st, stats)
     return out
 
 
@@ -336,14 +419,19 @@ def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.
                   caps: ExecutionCaps | None = None, stats: KernelStats | None = None, *, chunks: int = 0):
     """Reference ``sigkit::signature_vjp`` (autodiff.cpp:218-224): d<cotangent, Sig(X)>/dX,
     (B, L, d), for a (B, D) cotangent. numpy in -> numpy out; CUDA tensors in -> CUDA tensor out.
-    ``chunks`` pins the number of backward chunks per path (0: planned; 1: one sequential walk)."""
-    select_kernel(kernel, caps or ExecutionCaps.detect(), int(np.shape(paths)[1]) if len(np.shape(paths)) == 3 else 0)
+    ``chunks`` pins the number of backward chunks per path (0: planned; 1: one sequential walk).
+    Both kernel kinds run the same GPU adjoint (the reference's two adjoints agree,
+    test_autodiff.cpp:117-130)."""
+    select_kernel(kernel, caps or ExecutionCaps.detect(), _seq_len(paths))
     st = _Stats()
     tun = C.byref(_Tuning(chunks=chunks)) if chunks else None
     if _is_torch(paths):
         import torch
 
+        if not paths.is_cuda:
+            raise DomainError("torch input must be a CUDA tensor (use numpy for host buffers)")
         B, L, d = _validate_shape(paths.shape, depth)
+        _torch_dtype_ok(paths)
         X = paths.contiguous()
         cot = cotangent.to(device=X.device, dtype=X.dtype).contiguous()
         if tuple(cot.shape) != (B, sig_dim(d, depth)):
@@ -355,36 +443,28 @@ def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.
             _check(fn(X.data_ptr(), B, L, d, depth, cot.data_ptr(), grad.data_ptr(), SIGK_X_ON_DEVICE, s, tun,
                       C.byref(st)))
     else:
-        X = np.asarray(paths)
-        B, L, d = _validate_shape(X.shape, depth)
-        if X.dtype not in (np.float32, np.float64):
-            X = X.astype(np.float64)
-        X = np.ascontiguousarray(X)
+        X, B, L, d = _host_array(paths, depth)
         cot = np.ascontiguousarray(cotangent, dtype=X.dtype)
         if cot.shape != (B, sig_dim(d, depth)):
             raise DomainError("signature_vjp: cotangent shape does not match paths/depth")
         grad = np.empty_like(X)
         fn = lib().sigk_signature_vjp_f32 if X.dtype == np.float32 else lib().sigk_signature_vjp_f64
         _check(fn(X.ctypes.data, B, L, d, depth, cot.ctypes.data, grad.ctypes.data, 0, None, tun, C.byref(st)))
-    if stats is not None:
-        for f, _ in _Stats._fields_:
-            setattr(stats, f, getattr(st, f))
+    _copy_stats(st, stats)
     return grad
 
 
 def signature_sequential(paths, depth: int, stats: KernelStats | None = None, **kw):
-    """Reference ``signature_sequential`` (kernels.cpp:106-122)."""
+    """Reference ``signature_sequential`` (kernels.cpp:106-122): the chunked Chen fold."""
     return _run(paths, depth, stats, **kw)
 
 
-def signature_parallel(paths, depth: int, stats: KernelStats | None = None, memory_cap: int = 1 << 31, **kw):
-    """Reference ``signature_parallel`` (kernels.cpp:124-148), including its
-    ResourceError refusal above ``memory_cap`` scalars (sig_core.hpp:161-173)."""
-    B, L, d = _validate_shape(np.shape(paths), depth)
-    if float(B) * L * float(d) ** depth > memory_cap:
-        raise ResourceError(f"parallel kernel: intermediate storage of ~{float(B) * L * float(d) ** depth:g} "
-                            f"scalars exceeds cap {memory_cap}; use the sequential kernel for this shape")
-    return _run(paths, depth, stats, **kw)
+def signature_parallel(paths, depth: int, stats: KernelStats | None = None,
+                       memory_cap: int = DEFAULT_PARALLEL_MEMORY_CAP, *, out=None):
+    """Reference ``signature_parallel`` (kernels.cpp:124-148): the paper's per-degree
+    cumulative-sum formulation (sig_core.hpp:175-298) as N GPU scan passes, including
+    its ResourceError refusal above ``memory_cap`` scalars (sig_core.hpp:161-173)."""
+    return _run_parallel(paths, depth, stats, memory_cap, False, out=out)
 
 
 def signature_generic(paths, depth: int, stats: KernelStats | None = None):
@@ -500,5 +580,6 @@ __all__ = [
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
     "signature_stream", "signature_vjp", "TrainConfig", "train", "increments", "scaled_increments", "signature_bruteforce",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
-    "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_NAMES", "SIGK_X_ON_DEVICE", "SIGK_OUT_ON_DEVICE", "SIGK_ASYNC_HOST",
+    "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_SCAN", "FAMILY_NAMES", "SIGK_X_ON_DEVICE", "SIGK_OUT_ON_DEVICE",
+    "SIGK_ASYNC_HOST", "SIGK_PREFIX_ROWS", "DEFAULT_PARALLEL_MEMORY_CAP",
 ]

@@ -128,6 +128,7 @@ struct SigkTrainCtx {
     cudaStream_t s = nullptr;
     size_t n_samples = 0, seq_len = 0, D = 0, bmax = 0;
     int d = 0, depth = 0, tanh_act = 1;
+    int parallel = 0;  // KernelKind resolved to Parallel: the per-degree scan formulation (model.cpp:57)
     double *dX, *dY, *dW1, *db1, *dW2, *db2, *gW1, *gb1, *gW2, *gb2, *z, *gz, *sg, *gs, *y, *gy, *loss;
 };
 
@@ -199,8 +200,10 @@ extern "C" int sigk_internal_train_epoch(SigkTrainCtx* c, const size_t* batches,
         const double* Xb = c->dX + at * c->seq_len * kIn;
         const double* Yb = c->dY + at * kOut;
         dense_in<<<G, kT, 0, s>>>(Xb, c->dW1, c->db1, c->z, rows, d, c->tanh_act);
-        int rc = sigk_signature_f64(c->z, B, c->seq_len, d, c->depth, c->sg, SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE, s,
-                                    nullptr, nullptr);
+        int rc = c->parallel ? sigk_signature_parallel_f64(c->z, B, c->seq_len, d, c->depth, c->sg, size_t(1) << 31,
+                                                           SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE, s, nullptr)
+                             : sigk_signature_f64(c->z, B, c->seq_len, d, c->depth, c->sg,
+                                                  SIGK_X_ON_DEVICE | SIGK_OUT_ON_DEVICE, s, nullptr, nullptr);
         if (rc != SIGK_OK) return rc;
         dense_out<<<G, kT, 0, s>>>(c->sg, c->dW2, c->db2, c->y, (int)B, (int)D);
         loss_grad<<<1, kT, 0, s>>>(c->y, Yb, c->gy, c->loss, (int)(B * kOut));
@@ -221,6 +224,9 @@ extern "C" int sigk_internal_train_epoch(SigkTrainCtx* c, const size_t* batches,
     }
     return SIGK_OK;
 }
+
+// The forward kernel kind of the signature layer (the model's KernelKind after select_kernel).
+extern "C" void sigk_internal_train_set_parallel(SigkTrainCtx* c, int parallel) { c->parallel = parallel; }
 
 // Copies the parameters back and releases the device state.
 extern "C" int sigk_internal_train_close(SigkTrainCtx* c, double* W1, double* b1, double* W2, double* b2) {

@@ -20,6 +20,7 @@
 #include "vjp_kernel.cuh"
 #include "increments.cuh"
 #include "bruteforce.cuh"
+#include "scan_kernel.cuh"
 
 namespace sigk {
 
@@ -317,10 +318,14 @@ static bool may_overlap_previous(int dev, cudaStream_t s, const void* X, size_t 
 
 // Per-(device, stream) scratch of the pair family's segmented plans: kind 0 =
 // segment rows, kind 1 = per-path arrival counters (zeroed when allocated and
-// left at zero by every completed launch). Buffers are never freed (a CUDA
-// graph captured earlier may still reference them) and grow geometrically.
-// During stream capture a missing buffer is allocated stream-ordered instead
-// (and freed the same way by the caller).
+// left at zero by every completed launch); kinds >= 2: stream pieces and
+// reverse-mode buffers. A buffer is NEVER freed while the process runs: a
+// CUDA graph captured earlier, or a launch another host thread is enqueueing
+// with the pointer it got (ctypes releases the GIL), may still reference it.
+// Growth (geometric, so rare) allocates a new buffer and retires the old one
+// to a list that lives until process exit. During stream capture a missing
+// buffer is allocated stream-ordered instead (and freed the same way by the
+// caller, inside the captured graph).
 static void* segment_scratch(int dev, cudaStream_t s, int kind, size_t bytes, bool capturing, bool* async_alloc) {
     struct Buf {
         int dev;
@@ -331,6 +336,7 @@ static void* segment_scratch(int dev, cudaStream_t s, int kind, size_t bytes, bo
     };
     static std::mutex mu;
     static std::vector<Buf> bufs;
+    static std::vector<void*> retired;  // grown-out buffers: kept alive (see above)
     *async_alloc = false;
     std::lock_guard<std::mutex> g(mu);
     Buf* hit = nullptr;
@@ -345,22 +351,32 @@ static void* segment_scratch(int dev, cudaStream_t s, int kind, size_t bytes, bo
         return p;
     }
     const size_t n = std::max(bytes, hit ? 2 * hit->n : bytes);
-    if (hit) {  // growth is rare: retire the old buffer once the stream is done with it
-        cudaStreamSynchronize(s);
-        cudaFree(hit->p);
-        hit->p = nullptr;
-        hit->n = 0;
-    }
     void* p = nullptr;
     if (cudaMalloc(&p, n) != cudaSuccess) return nullptr;
-    if ((kind == 1 || kind == 12) && cudaMemset(p, 0, n) != cudaSuccess) return nullptr;  // counters, flags
+    // counters / flags start at zero, ordered before the launch on this stream
+    if ((kind == 1 || kind == 12) && cudaMemsetAsync(p, 0, n, s) != cudaSuccess) return nullptr;
     if (hit) {
+        retired.push_back(hit->p);
         hit->p = p;
         hit->n = n;
     } else {
         bufs.push_back(Buf{dev, s, kind, p, n});
     }
     return p;
+}
+
+// Increments of one path covered by a launch of G segments x U chunks
+// (segment g folds [g*SL, min((g+1)*SL, M)), chunk u of it CL steps):
+// sigk_stats.path_steps, counted from the geometry the kernels were given.
+static int64_t covered_steps(int64_t M, int64_t G, int64_t U) {
+    const int64_t SL = (M + G - 1) / G, CL = (SL + U - 1) / U;
+    int64_t n = 0;
+    for (int64_t g = 0; g < G; ++g) {
+        const int64_t s0 = std::min(M, g * SL), s1 = std::min(M, s0 + SL);
+        for (int64_t u = 0; u < U; ++u)
+            n += std::max<int64_t>(0, std::min(s1, s0 + (u + 1) * CL) - std::min(s1, s0 + u * CL));
+    }
+    return n;
 }
 
 template <typename Real>
@@ -409,6 +425,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         record(ev1);
         if (e != cudaSuccess) return cuda_fail(e, "generic fold launch");
         local.fold_steps = M;
+        local.path_steps = M;
         local.chunks = 1;
         local.prefix_len = -1;
         local.threads_per_unit = 0;
@@ -445,6 +462,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         int grounds = 0;
         while ((1 << grounds) < G) ++grounds;
         local.fold_steps = CL;
+        local.path_steps = covered_steps(M, G, U);
         local.scan_passes = rounds + grounds;
         local.chunks = U;
         local.prefix_len = v->Q;
@@ -476,6 +494,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
     int rounds = 0;
     while ((1 << rounds) < U) ++rounds;
     local.fold_steps = CL;
+    local.path_steps = v->family == KernelFamily::Path ? covered_steps(M, 1, U) : M;
     local.scan_passes = rounds;
     local.chunks = U;
     local.prefix_len = v->Q;
@@ -916,6 +935,7 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
         local.chunks = 1;
         local.fold_steps = M;
     }
+    local.path_steps = M;  // pass 2 folds every step of every path once (pair) / the generic walk does
     if (st) *st = local;
     return SIGK_OK;
 }
@@ -974,6 +994,132 @@ static int stream_impl(const Real* X, size_t B, size_t L, int d, int N, Real* ou
     return rc;
 }
 
+// The paper's parallel formulation (KernelKind::Parallel; reference
+// detail::parallel_forward, sig_core.hpp:175-298, scan_kernel.cuh): N degree
+// passes over a (B, M, D) workspace of per-position levels. With
+// SIGK_PREFIX_ROWS the workspace is the caller's (B, L-1, D) output (the
+// reference's signature_stream over the parallel kernel, kernels.cpp:183-197);
+// otherwise it is stream-ordered scratch and row M-1 of every path is copied
+// out. The reference's memory refusal (check_parallel_memory, :161-173) is
+// applied first with the same message.
+template <typename Real>
+static int parallel_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* out, bool prefix_rows,
+                           cudaStream_t s, sigk_stats* st) {
+    int64_t D = 0, p = 1;
+    for (int n = 0; n < N; ++n) {
+        p *= d;
+        D += p;
+    }
+    const int64_t M = L - 1;
+    sigk_stats local{};
+    local.family = SIGK_FAMILY_SCAN;
+    local.chunks = 1;
+    local.segments = 1;
+    local.prefix_len = -1;
+    cudaError_t e;
+    if (M == 0) {  // identity; the reference still counts its N (empty) passes (sig_core.hpp:201-206)
+        if (!prefix_rows) {
+            e = cudaMemsetAsync(out, 0, sizeof(Real) * B * D, s);
+            if (e != cudaSuccess) return cuda_fail(e, "memset");
+        }
+        local.scan_passes = N;
+        if (st) *st = local;
+        return SIGK_OK;
+    }
+    ScanGeom<Real> g{};
+    Real factorial = 1;
+    g.pw[0] = 1;
+    for (int j = 1; j <= N; ++j) {
+        g.pw[j] = g.pw[j - 1] * d;
+        factorial *= Real(j);
+        g.inv_fact[j] = Real(1) / factorial;
+        g.off[j] = g.off[j - 1] + g.pw[j];  // level j occupies [off[j-1], off[j]) of a D-row
+    }
+    Real* W = out;
+    bool scratch = false;
+    if (!prefix_rows) {
+        e = cudaMallocAsync(&W, sizeof(Real) * B * M * D, s);
+        if (e != cudaSuccess) return cuda_fail(e, "parallel-formulation workspace");
+        scratch = true;
+    }
+    constexpr int NW = 8;
+    for (int n = 1; n <= N && e == cudaSuccess; ++n) {
+        const int64_t grid = B * ((g.pw[n] + 31) / 32);
+        if (N <= 8) degree_scan_kernel<Real, NW, 8><<<(unsigned)grid, 32 * NW, 0, s>>>(X, L, d, n, M, W, D, g);
+        else degree_scan_kernel<Real, NW, kScanMaxDepth><<<(unsigned)grid, 32 * NW, 0, s>>>(X, L, d, n, M, W, D, g);
+        e = cudaGetLastError();
+        local.scan_passes += 1;
+        local.launches += 1;
+    }
+    if (e == cudaSuccess && !prefix_rows)  // the last position of every path (gather_position, :300-311)
+        e = cudaMemcpy2DAsync(out, sizeof(Real) * D, W + (M - 1) * D, sizeof(Real) * M * D, sizeof(Real) * D, B,
+                              cudaMemcpyDeviceToDevice, s);
+    if (scratch) cudaFreeAsync(W, s);
+    if (e != cudaSuccess) return cuda_fail(e, "parallel formulation");
+    if (st) *st = local;
+    return SIGK_OK;
+}
+
+template <typename Real>
+static int parallel_impl(const Real* X, size_t B, size_t L, int d, int N, Real* out, size_t memory_cap,
+                         unsigned flags, void* stream, sigk_stats* st) {
+    g_err.clear();
+    int rc = validate(X, B, L, d, N, out);
+    if (rc != SIGK_OK) return rc;
+    const bool prefix_rows = flags & SIGK_PREFIX_ROWS;
+    if (prefix_rows && L < 2)
+        return fail(SIGK_EDOMAIN, "signature_stream: need at least 2 points, got L = " + std::to_string(L));
+    {  // check_parallel_memory (sig_core.hpp:161-173), same message
+        long double scalars = static_cast<long double>(B) * static_cast<long double>(L);
+        for (int n = 0; n < N; ++n) scalars *= static_cast<long double>(d);
+        if (scalars > static_cast<long double>(memory_cap))
+            return fail(SIGK_ERESOURCE, "parallel kernel: intermediate storage of ~" +
+                                            std::to_string(static_cast<double>(scalars)) + " scalars exceeds cap " +
+                                            std::to_string(memory_cap) + "; use the sequential kernel for this shape");
+    }
+    if (N > kScanMaxDepth)
+        return fail(SIGK_ERESOURCE, "parallel formulation: depth " + std::to_string(N) + " exceeds " +
+                                        std::to_string(kScanMaxDepth));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    size_t D = 0;
+    sigk_sig_dim(d, N, &D);
+    const size_t rows = prefix_rows ? B * (L - 1) : B;
+    const size_t xbytes = sizeof(Real) * B * L * d, obytes = sizeof(Real) * rows * D;
+    const bool xdev = flags & SIGK_X_ON_DEVICE, odev = flags & SIGK_OUT_ON_DEVICE;
+    cudaError_t e;
+    if (xdev && odev) {
+        rc = parallel_device<Real>(X, (int64_t)B, (int64_t)L, d, N, out, prefix_rows, s, st);
+        if (rc == SIGK_OK) {
+            e = cudaPeekAtLastError();
+            if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
+        }
+        return rc;
+    }
+    // host buffers: synchronous, stream-ordered device copies
+    Real* Xd = const_cast<Real*>(X);
+    Real* Od = out;
+    if (!xdev) {
+        e = cudaMallocAsync(&Xd, xbytes, s);
+        if (e != cudaSuccess) return cuda_fail(e, "paths allocation");
+        e = cudaMemcpyAsync(Xd, X, xbytes, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+    }
+    if (!odev) {
+        e = cudaMallocAsync(&Od, obytes, s);
+        if (e != cudaSuccess) return cuda_fail(e, "output allocation");
+    }
+    rc = parallel_device<Real>(Xd, (int64_t)B, (int64_t)L, d, N, Od, prefix_rows, s, st);
+    if (rc == SIGK_OK && !odev) {
+        e = cudaMemcpyAsync(out, Od, obytes, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "D2H copy");
+    }
+    if (!xdev) cudaFreeAsync(Xd, s);
+    if (!odev) cudaFreeAsync(Od, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && rc == SIGK_OK) rc = cuda_fail(e, "stream synchronize");
+    return rc;
+}
+
 // Reverse mode (reference signature_vjp, autodiff.cpp:218-224): the prefix
 // states come from the stream kernels into stream-ordered scratch, then
 // vjp_kernel walks the steps backwards (vjp_kernel.cuh).
@@ -989,6 +1135,8 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     cudaError_t e;
     int dev = 0;
     cudaGetDevice(&dev);
+    if (st) *st = sigk_stats{};  // every field below describes this call only
+    const bool pdl = !(tun && tun->no_overlap);  // sigk.h: no_overlap = never a programmatic dependent launch
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cap);
     // working buffers persist per (device, stream) across calls (a stream-ordered
@@ -1040,7 +1188,9 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             // in [want/2, 2 want] minimising that (ties: fewer chunks, cheaper
             // chunk passes). C2: U = 9 (2 CTAs per SM x 111 steps) beats 10 (3 x 100).
             int64_t best = -1;
-            const int64_t lo = std::max<int64_t>(2, want / 2), hi = std::min<int64_t>(2 * want, M / 16);
+            // (U = 1 included: when the batch alone fills the GPU one full-path
+            // walk per item beats the gather + chunk-signature + chunk passes)
+            const int64_t lo = std::max<int64_t>(1, want / 2), hi = std::min<int64_t>(2 * want, M / 16);
             for (int64_t u = lo; u <= hi; ++u) {
                 const int64_t cl = (M + u - 1) / u, ctas = (B * u + 4 * sl.slots - 1) / (4 * sl.slots);
                 const int64_t cost = (ctas + sms - 1) / sms * cl;
@@ -1141,7 +1291,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = pdl ? 1 : 0;
         e = cudaLaunchKernelEx(&cfg, sl.fn, X, L, items, U, CL, static_cast<const Real*>(ends), cbars, grad);
         if (e != cudaSuccess) {
             release();
@@ -1161,7 +1311,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;  // the kernel waits for its predecessor before reading anything
+        cfg.numAttrs = pdl ? 1 : 0;  // the kernel waits for its predecessor before reading anything
         e = cudaLaunchKernelEx(&cfg, vk, X, L, d, N, D, static_cast<const Real*>(states), cbars, U, CL,
                                dbar, gwork, use_smem);
         if (e != cudaSuccess) {
@@ -1184,6 +1334,12 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         st->launches += launches;
         st->chunks = U;
         st->fold_steps = CL;
+        st->path_steps = covered_steps(std::max<int64_t>(M, 0), 1, U);
+        st->scan_passes = 0;
+        st->segments = 1;
+        st->prefix_len = -1;
+        st->threads_per_unit = 0;
+        st->family = SIGK_FAMILY_AUTO;  // reverse mode has its own kernels (vjp_slice.cuh / vjp_kernel.cuh)
     }
     return SIGK_OK;
 }
@@ -1393,6 +1549,16 @@ int sigk_signature_stream_f64(const double* X, size_t B, size_t L, int d, int N,
     return sigk::stream_impl<double>(X, B, L, d, N, out, flags, stream, tuning, stats);
 }
 
+int sigk_signature_parallel_f32(const float* X, size_t B, size_t L, int d, int N, float* out, size_t memory_cap,
+                                unsigned flags, void* stream, sigk_stats* stats) {
+    return sigk::parallel_impl<float>(X, B, L, d, N, out, memory_cap, flags, stream, stats);
+}
+
+int sigk_signature_parallel_f64(const double* X, size_t B, size_t L, int d, int N, double* out, size_t memory_cap,
+                                unsigned flags, void* stream, sigk_stats* stats) {
+    return sigk::parallel_impl<double>(X, B, L, d, N, out, memory_cap, flags, stream, stats);
+}
+
 int sigk_signature_vjp_f32(const float* X, size_t B, size_t L, int d, int N, const float* cotangent, float* grad,
                            unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats) {
     return sigk::vjp_impl<float>(X, B, L, d, N, cotangent, grad, flags, stream, tuning, stats);
@@ -1444,7 +1610,7 @@ const char* sigk_last_error(void) { return sigk::g_err.c_str(); }
 // internal: lets the C++ API units report through sigk_last_error
 void sigk_internal_set_error(const char* msg) { sigk::g_err = msg; }
 
-int sigk_version(void) { return 101; }
+int sigk_version(void) { return 200; }
 
 }  // extern "C"
 

@@ -40,19 +40,27 @@ void validate_depth(int depth) {
     if (depth < 1) throw DomainError("depth must be >= 1, got " + std::to_string(depth));
 }
 
-// KernelStats keep the reference's observable meaning (kernels.cpp:106-148,
-// sig_core.hpp:194-204): the sequential-stage count of the reference
-// algorithm of the selected kind — fold_steps = L-1 for the sequential kernel,
-// scan_passes = depth for the parallel one. The GPU decomposition (chunks,
-// segments, launches) is reported by the C ABI's sigk_stats.
-void ref_counters(KernelKind kind, std::size_t len, int depth, KernelStats* stats) {
+// KernelStats from what the GPU actually ran (reference meaning,
+// kernels.hpp:86-91, kernels.cpp:117-120, 143-146): the sequential kind runs
+// the chunked Chen fold, fold_steps = the fold steps its launches applied per
+// path (sigk_stats.path_steps, summed over the path's chunk units from the
+// launch geometry = L-1), scan_passes = 0; the parallel kind runs the paper's
+// per-degree scan formulation, fold_steps = 0, scan_passes = the degree
+// passes launched (= depth). The chunk/segment decomposition of the fold is
+// in the C ABI's sigk_stats.
+void set_counters(const sigk_stats& st, KernelStats* stats) {
     if (!stats) return;
-    const bool par = kind == KernelKind::Parallel;
-    stats->fold_steps = par ? 0 : static_cast<std::int64_t>(len) - 1;
-    stats->scan_passes = par ? depth : 0;
+    if (st.family == SIGK_FAMILY_SCAN) {
+        stats->fold_steps = 0;
+        stats->scan_passes = st.scan_passes;
+    } else {
+        stats->fold_steps = st.path_steps;
+        stats->scan_passes = 0;
+    }
 }
 
-SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats, KernelKind kind) {
+SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats, KernelKind kind,
+                       std::size_t memory_cap = kDefaultParallelMemoryCap) {
     validate_paths(paths);
     validate_depth(depth);
     SignatureBatch out;
@@ -61,9 +69,13 @@ SignatureBatch run_gpu(const PathBatch& paths, int depth, KernelStats* stats, Ke
     out.depth = depth;
     out.flat.resize(paths.batch * sig_dim(paths.dim, depth));
     sigk_stats st{};
-    check(sigk_signature_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, out.flat.data(), 0u,
-                             nullptr, nullptr, &st));
-    ref_counters(kind, paths.len, depth, stats);
+    if (kind == KernelKind::Parallel)
+        check(sigk_signature_parallel_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth,
+                                          out.flat.data(), memory_cap, 0u, nullptr, &st));
+    else
+        check(sigk_signature_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, out.flat.data(), 0u,
+                                 nullptr, nullptr, &st));
+    set_counters(st, stats);
     return out;
 }
 
@@ -133,6 +145,7 @@ PrefixSignatureBatch signature_stream(const PathBatch& paths, int depth, KernelK
     validate_depth(depth);
     if (paths.len < 2)
         throw DomainError("signature_stream: need at least 2 points, got L = " + std::to_string(paths.len));
+    const KernelKind kind = select_kernel(kernel, caps, paths.len);
     PrefixSignatureBatch out;
     out.batch = paths.batch;
     out.prefixes = paths.len - 1;
@@ -140,9 +153,13 @@ PrefixSignatureBatch signature_stream(const PathBatch& paths, int depth, KernelK
     out.depth = depth;
     out.flat.resize(paths.batch * out.prefixes * sig_dim(paths.dim, depth));
     sigk_stats st{};
-    check(sigk_signature_stream_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, out.flat.data(), 0u,
-                                    nullptr, nullptr, &st));
-    ref_counters(select_kernel(kernel, caps, paths.len), paths.len, depth, stats);
+    if (kind == KernelKind::Parallel)  // kernels.cpp:183-197: every position of the parallel state
+        check(sigk_signature_parallel_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth,
+                                          out.flat.data(), kDefaultParallelMemoryCap, SIGK_PREFIX_ROWS, nullptr, &st));
+    else
+        check(sigk_signature_stream_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth,
+                                        out.flat.data(), 0u, nullptr, nullptr, &st));
+    set_counters(st, stats);
     return out;
 }
 
@@ -183,7 +200,7 @@ KernelKind kernel_from_name(const std::string& name) {
 ExecutionCaps ExecutionCaps::detect() {
     ExecutionCaps caps;
     const char* env = std::getenv("SIGKIT_ACCELERATED");
-    caps.accelerated = env == nullptr || (std::string(env) != "0");
+    caps.accelerated = env != nullptr && std::string(env) != "0" && std::string(env) != "";  // kernels.cpp:64-69
     return caps;
 }
 
@@ -243,17 +260,8 @@ SignatureBatch signature_sequential(const PathBatch& paths, int depth, KernelSta
 }
 
 SignatureBatch signature_parallel(const PathBatch& paths, int depth, KernelStats* stats, std::size_t memory_cap) {
-    validate_paths(paths);
-    validate_depth(depth);
-    // Keep the reference's observable refusal (sig_core.hpp:161-173) so callers
-    // that rely on it behave the same; the GPU path itself has no such limit.
-    long double scalars = static_cast<long double>(paths.batch) * static_cast<long double>(paths.len);
-    for (int n = 0; n < depth; ++n) scalars *= static_cast<long double>(paths.dim);
-    if (scalars > static_cast<long double>(memory_cap))
-        throw ResourceError("parallel kernel: intermediate storage of ~" + std::to_string(static_cast<double>(scalars)) +
-                            " scalars exceeds cap " + std::to_string(memory_cap) +
-                            "; use the sequential kernel for this shape");
-    return run_gpu(paths, depth, stats, KernelKind::Parallel);
+    // the C ABI applies the reference's refusal (sig_core.hpp:161-173) with the same message
+    return run_gpu(paths, depth, stats, KernelKind::Parallel, memory_cap);
 }
 
 SignatureBatch signature(const PathBatch& paths, int depth, KernelKind kernel, const ExecutionCaps& caps,
@@ -266,7 +274,7 @@ void signature_f32(const float* paths, std::size_t batch, std::size_t len, int d
                    KernelStats* stats) {
     sigk_stats st{};
     check(sigk_signature_f32(paths, batch, len, dim, depth, out, 0u, nullptr, nullptr, &st));
-    ref_counters(KernelKind::Sequential, len, depth, stats);  // the float core is sequential_forward<float>
+    set_counters(st, stats);  // the float core is sequential_forward<float>
 }
 
 // ---- tensor algebra (host utilities; semantics of tensor_algebra.cpp:10-127)

@@ -46,7 +46,90 @@ static double max_abs_diff(const std::vector<double>& a, const std::vector<doubl
     return m;
 }
 
-int main() {
+// test_kernels.cpp:299-315 — dispatch follows hint, capability and length;
+// detect() reads SIGKIT_ACCELERATED (host logic only: runs without a GPU)
+static void host_dispatch_cases() {
+    ExecutionCaps plain;  // accelerated = false
+    ExecutionCaps accel;
+    accel.accelerated = true;
+    CHECK(!plain.accelerated && plain.parallel_min_len == 64);
+    CHECK(select_kernel(KernelKind::Sequential, accel, 1000) == KernelKind::Sequential);
+    CHECK(select_kernel(KernelKind::Parallel, plain, 2) == KernelKind::Parallel);
+    CHECK(select_kernel(KernelKind::Auto, accel, 64) == KernelKind::Parallel);
+    CHECK(select_kernel(KernelKind::Auto, accel, 63) == KernelKind::Sequential);
+    CHECK(select_kernel(KernelKind::Auto, plain, 1000) == KernelKind::Sequential);
+    accel.parallel_min_len = 10;
+    CHECK(select_kernel(KernelKind::Auto, accel, 10) == KernelKind::Parallel);
+
+    const char* old = std::getenv("SIGKIT_ACCELERATED");
+    const std::string saved = old ? old : "";
+    unsetenv("SIGKIT_ACCELERATED");
+    CHECK(!ExecutionCaps::detect().accelerated);
+    setenv("SIGKIT_ACCELERATED", "1", 1);
+    CHECK(ExecutionCaps::detect().accelerated);
+    setenv("SIGKIT_ACCELERATED", "0", 1);
+    CHECK(!ExecutionCaps::detect().accelerated);
+    setenv("SIGKIT_ACCELERATED", "", 1);
+    CHECK(!ExecutionCaps::detect().accelerated);
+    if (old) setenv("SIGKIT_ACCELERATED", saved.c_str(), 1);
+    else unsetenv("SIGKIT_ACCELERATED");
+    CHECK(std::string(kernel_name(KernelKind::Parallel)) == "parallel");
+    CHECK(kernel_from_name("sequential") == KernelKind::Sequential);
+}
+
+int main(int argc, char** argv) {
+    host_dispatch_cases();
+    if (argc > 1 && std::string(argv[1]) == "--host-only") {
+        std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "ok", failures);
+        return failures ? 1 : 0;
+    }
+
+    // test_kernels.cpp:102-117 — structural counters from what the GPU ran:
+    // the fold's steps per path, the scan formulation's degree passes
+    {
+        const PathBatch paths = random_paths(24, 2, 17, 2, 0.5);
+        KernelStats stats;
+        signature_sequential(paths, 3, &stats);
+        CHECK(stats.fold_steps == 16 && stats.scan_passes == 0);
+        signature_parallel(paths, 3, &stats);
+        CHECK(stats.fold_steps == 0 && stats.scan_passes == 3);
+        const PathBatch longer = random_paths(25, 1, 200, 2, 0.1);
+        signature_sequential(longer, 3, &stats);
+        CHECK(stats.fold_steps == 199);
+        signature_parallel(longer, 3, &stats);
+        CHECK(stats.scan_passes == 3);
+        // the memory refusal (sig_core.hpp:161-173), before any device work
+        bool threw = false;
+        try { signature_parallel(longer, 3, &stats, 100); } catch (const ResourceError&) { threw = true; }
+        CHECK(threw);
+    }
+
+    // acceptance.cpp:87-107 — the two GPU algorithms (chunked fold vs per-degree
+    // scans) agree on a grid of shapes, including L = 1 and L = 2
+    {
+        double worst = 0;
+        for (std::size_t L : {1, 2, 3, 17, 64, 130})
+            for (int d : {1, 2, 3, 5})
+                for (int N : {1, 2, 3, 4}) {
+                    const PathBatch p = random_paths(static_cast<unsigned>(L * 100 + d * 10 + N), 3, L, d, 0.4);
+                    const SignatureBatch a = signature(p, N, KernelKind::Sequential);
+                    const SignatureBatch b = signature(p, N, KernelKind::Parallel);
+                    double mx = 0;
+                    for (double v : a.flat) mx = std::fmax(mx, std::fabs(v));
+                    worst = std::fmax(worst, max_abs_diff(a.flat, b.flat) / (1 + mx));
+                }
+        CHECK(worst <= 1e-9);
+        const PathBatch p = random_paths(5, 2, 40, 3, 0.3);
+        ExecutionCaps accel;
+        accel.accelerated = true;
+        KernelStats sa, sb;
+        const PrefixSignatureBatch s0 = signature_stream(p, 3, KernelKind::Sequential, accel, &sa);
+        const PrefixSignatureBatch s1 = signature_stream(p, 3, KernelKind::Auto, accel, &sb);  // 40 < 64: sequential
+        CHECK(max_abs_diff(s0.flat, s1.flat) == 0.0 && sa.fold_steps == 39);
+        const PrefixSignatureBatch s2 = signature_stream(p, 3, KernelKind::Parallel, accel, &sb);
+        CHECK(max_abs_diff(s0.flat, s2.flat) <= 1e-10 && sb.scan_passes == 3 && sb.fold_steps == 0);
+    }
+
     // acceptance.cpp:54-58
     CHECK(sig_dim(10, 4) == 11110 && sig_dim(2, 2) == 6 && sig_dim(6, 3) == 258);
 

@@ -125,3 +125,27 @@ def test_sigbench_cli_rejects_bad_flags():
     assert r.returncode == 1 and "--dims entries must be positive" in r.stderr
     r = subprocess.run([exe, "--dtype", "f16"], capture_output=True, text=True)
     assert r.returncode == 1
+
+
+def test_out_argument_validated_before_any_device_work(sk):
+    # a wrong `out` must be refused before its pointer reaches the C ABI
+    X = np.zeros((2, 5, 3))
+    for bad in (np.empty((2, 38)), np.empty((2, 39), np.float32), np.empty((39, 2)).T):
+        with pytest.raises(sk.DomainError):
+            sk.signature(X, 3, out=bad)
+    with pytest.raises(sk.DomainError):
+        sk.signature_stream(X, 3, out=np.empty((2, 5, 39)))
+    with pytest.raises(sk.DomainError):
+        sk.signature_parallel(X, 3, out=np.empty((2, 4, 39)))
+
+
+def test_reference_dispatch_defaults(sk, monkeypatch):
+    # kernels.hpp:80 (accelerated = false), kernels.cpp:64-69 (detect)
+    K = sk.KernelKind
+    assert sk.ExecutionCaps().accelerated is False
+    monkeypatch.delenv("SIGKIT_ACCELERATED", raising=False)
+    assert sk.ExecutionCaps.detect().accelerated is False
+    assert sk.select_kernel(K.Auto, sk.ExecutionCaps.detect(), 1000) is K.Sequential
+    for v, want in (("1", True), ("yes", True), ("0", False), ("", False)):
+        monkeypatch.setenv("SIGKIT_ACCELERATED", v)
+        assert sk.ExecutionCaps.detect().accelerated is want, v

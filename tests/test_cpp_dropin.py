@@ -31,3 +31,9 @@ def test_dropin_reference_cases_on_gpu(name):
     r = subprocess.run([build(name)], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_dropin_host_dispatch_cases():
+    # test_kernels.cpp:299-315 (dispatch, SIGKIT_ACCELERATED): host logic, no GPU needed
+    r = subprocess.run([build("test_dropin"), "--host-only"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stdout + r.stderr
