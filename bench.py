@@ -6,21 +6,30 @@
 A "step" is one pass of the hot path (sigk_signature_f32 through the C ABI)
 over one batch. Default workload = BASELINE.json configs[1]: B=128 paths,
 L=1000, d=5, depth N=4, fp32, synthetic Brownian paths (X0 = 0, increments
-N(0, 1/(L-1)), Philox keyed by (seed, row, t, c)). Under torchrun each rank
-processes its own B=128 rows (weak scaling, no data-path collective); timings
-are the max over ranks.
+N(0, 1/(L-1)), Philox keyed by (seed, global row, t, c)). Multi-GPU (torchrun,
+one rank per GPU, no data-path collective, timings = max over ranks):
+c1..c4 are weak-scaled (every rank folds its own B rows); c5 (BASELINE.json
+configs[4], "batch sharded across 1/2/4/8 B200") is strong-scaled: the global
+B = 8192 batch is split into contiguous row shards (rank_rows, the split of
+sigk_signature_sharded_*), so N=1 is exactly the single-GPU c5 run.
 
-value  : device-resident inputs (a pool of input batches larger than the
-         126 MB L2, rotated every step), K steps captured in CUDA graphs and
-         replayed on one stream, CUDA events around the whole region.
+value  : device-resident inputs, K steps captured in CUDA graphs and replayed
+         on one stream, CUDA events around the whole region. Every timed step
+         reads a distinct input batch of a pool that rotates through more than
+         2x the 126 MB L2, and L2 is flushed (a 512 MiB device write) right
+         before the timed region, so inputs come from HBM even at small K.
 e2e    : the same call with HOST (pinned) buffers: H2D of the step's paths,
-         kernels, D2H of the step's signatures, every step.
-roofline: the fold kernel (the dominant kernel) timed with CUDA events on its
-         launch stream inside the timed graphs; achieved = credited FP32 flops
-         per launch / mean fold duration, against an FFMA-pipe peak measured
-         on this GPU by a register-resident microbenchmark.
+         kernels, D2H of the step's signatures, every step (PCIe link rates
+         reported beside it).
+roofline: achieved = credited FP32 flops per step / mean step interval of the
+         timed replays (back-to-back launches may overlap through programmatic
+         dependent launch); `single_call` = the same credited flops over the
+         fold kernel's own duration with no launch overlap (CUDA events around
+         single launches inside an untimed graph replay). Peak = FFMA-pipe
+         rate measured on this GPU by a register-resident microbenchmark.
 cpu_baseline: the reference's own sequential_forward<double> compiled from its
-         sources (oracle/_ref; else the C port), all host threads, rank 0 only.
+         sources (oracle/_ref; else the C port), all host threads, rank 0 only;
+         `variants` adds 1 thread (as shipped) and the <float> instantiation.
 """
 from __future__ import annotations
 
@@ -58,6 +67,33 @@ def work_per_path(L, d, N):
     W = sum((N - k + 1) * d ** k for k in range(1, N + 1))
     D = sum(d ** n for n in range(1, N + 1))
     return 2.0 * W * (L - 1), 4.0 * (L * d + D), W, D
+
+
+def rank_rows(config: str, world: int, rank: int):
+    """(global batch, first row, row count, scaling) of `rank` for a config: c5
+    is strong-scaled over contiguous row shards (shard_rows: the split of
+    sigk_signature_sharded_*); the other configs give every rank its own B rows
+    (weak scaling, rows rank*B ..)."""
+    from paper_2501_08455_b200.shard import shard_rows
+
+    B = CONFIGS[config][0]
+    if config == "c5":
+        lo, hi = shard_rows(B, world, rank)
+        return B, lo, hi - lo, "strong"
+    return B * world, rank * B, B, "weak"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def load_peaks():
@@ -190,27 +226,46 @@ def cpu_reference_run(X64, N, threads):
     return time.perf_counter() - t0, kind
 
 
-def cpu_baseline(X32, N, budget_s=6.0):
+def cpu_timed(X, N, threads, budget_s):
+    """Best paths/s of repeated reference passes over a bounded row sample of X
+    (f64 or f32: the reference's sequential_forward<double> / <float>)."""
+    B = X.shape[0]
+    w = max(1, min(B, threads))
+    t1, kind = cpu_reference_run(X[:w], N, threads)  # one wave of `threads` rows
+    rows = int(max(w, min(B, w * max(1, int(min(1.0, budget_s / 4) / max(t1, 1e-9))))))
+    Xs = X[:rows]
+    best, total, reps = float("inf"), 0.0, 0
+    while (total < budget_s and reps < 1000) or reps == 0:
+        dt, kind = cpu_reference_run(Xs, N, threads)
+        best, total, reps = min(best, dt), total + dt, reps + 1
+    return rows / best, rows, reps, total, kind
+
+
+def cpu_baseline(X32, N, budget_s=6.0, variants=True):
     """Reference sequential_forward<double> (what signature_sequential runs) on the
-    same fp32 inputs promoted to double, all host threads, repeated ~budget_s."""
+    same fp32 inputs promoted to double, all host threads, repeated ~budget_s;
+    plus 1 thread (the reference as shipped, README.md:65) and <float>
+    (bench.cpp:29-56, 182-186) variants on bounded samples."""
     import numpy as np
 
     threads = os.cpu_count() or 1
     X64 = X32.astype(np.float64)
     B = X64.shape[0]
-    # bound the sample: at most ~1 s per pass
-    t1, kind = cpu_reference_run(X64[: max(1, min(B, threads))], N, threads)
-    per_row = t1 / max(1, min(B, threads)) * threads
-    rows = int(min(B, max(threads, 1.0 / max(per_row / threads, 1e-9))))
-    rows = max(1, min(B, rows))
-    Xs = X64[:rows]
-    best, total, reps = float("inf"), 0.0, 0
-    while total < budget_s and reps < 1000:
-        dt, kind = cpu_reference_run(Xs, N, threads)
-        best, total, reps = min(best, dt), total + dt, reps + 1
-    return {"value": rows / best, "unit": "paths/s", "cores": threads, "kind": kind,
-            "sample": f"{rows} of {B} rows, best of {reps} passes ({total:.1f} s wall)",
-            "seconds_best": best}
+    v, rows, reps, total, kind = cpu_timed(X64, N, threads, budget_s)
+    out = {"value": v, "unit": "paths/s", "cores": threads, "kind": kind,
+           "sample": f"{rows} of {B} rows, best of {reps} passes ({total:.1f} s wall), f64, {threads} threads",
+           "cpu_model": cpu_model()}
+    if variants:
+        var = []
+        for prec, Xv in (("f64", X64), ("f32", np.ascontiguousarray(X32, np.float32))):
+            for th in sorted({1, threads}):
+                if prec == "f64" and th == threads:
+                    continue  # the headline figure above
+                vv, r, n, t, k = cpu_timed(Xv, N, th, budget_s / 3)
+                var.append({"value": vv, "unit": "paths/s", "threads": th, "precision": prec, "kind": k,
+                            "sample": f"{r} rows, best of {n} passes ({t:.1f} s)"})
+        out["variants"] = var
+    return out
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -228,17 +283,21 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    B, L, d, N = CONFIGS[args.config]
+    _, L, d, N = CONFIGS[args.config]
+    B_global, row0, B, scaling = rank_rows(args.config, world, rank)
+    if scaling == "strong":
+        TUNE["plan_rows"] = B_global  # same plan (hence bitwise the same rows) for any GPU count
     flops_path, bytes_path, W, D = work_per_path(L, d, N)
     stream = torch.cuda.Stream(device=dev)
 
-    # input pool larger than L2 (rotated every step), distinct rows per rank
+    # input pool of more than 2x L2 (rotated every step), this rank's global rows
     in_bytes = B * L * d * 4
     n_buf = 2 if in_bytes > L2_BYTES else min(256, math.ceil(2 * L2_BYTES / in_bytes))
     pool = torch.empty((n_buf, B, L, d), dtype=torch.float32, device=dev)
     with torch.cuda.stream(stream):
         for i in range(n_buf):
-            sk.brownian(pool[i], seed=42 + i, row0=rank * B)
+            sk.brownian(pool[i], seed=42 + i, row0=row0)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev)  # > 4x L2
     out = torch.empty((B, D), dtype=torch.float32, device=dev)
     stream.synchronize()
 
@@ -301,6 +360,7 @@ def run_ours(args):
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with clk:
         with torch.cuda.stream(stream):
+            flush.fill_(1.0)  # evict the warm-up's inputs from L2 (untimed)
             t0.record(stream)
             for _ in range(reps_full):
                 g_main.replay()
@@ -312,6 +372,7 @@ def run_ours(args):
     barrier(world)
     elapsed = max_over_ranks(t0.elapsed_time(t1) * 1e-3, world)
     with torch.cuda.stream(stream):
+        flush.fill_(2.0)
         g_ev.replay()
     stream.synchronize()
     fold_ms = [a.elapsed_time(b) for a, b in ev_main]
@@ -383,8 +444,12 @@ def run_ours(args):
             dist.destroy_process_group()
         return
     steps = args.steps
-    value = world * B * steps / elapsed
+    B_all = B_global if scaling == "strong" else world * B  # rows all ranks processed per step
+    value = B_all * steps / elapsed
+    # credited flops of this rank's step (the slowest rank bounds the step interval)
     achieved = B * flops_path / (elapsed / steps) / 1e12
+    single_tf = B * flops_path / fold_s / 1e12
+    e2e_h2d, e2e_d2h = in_bytes, B * D * 4
     kernel_name = {1: "path_kernel", 2: "flat_kernel", 3: "pair_kernel", 4: "generic_fold_kernel",
                    5: "ipair_kernel"}.get(st.family, "?")
     traffic = _traffic(args.config)
@@ -398,22 +463,27 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": elapsed / steps * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling,
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic Brownian paths (Philox, X0=0, N(0,1/(L-1)) increments), generated on device",
         "config": {
-            "workload": f"{args.config}: B={B} L={L} d={d} N={N} fp32 batched truncated signature per GPU"
-                        + (" (BASELINE.json configs[1], headline)" if args.config == "c2" else ""),
-            "batch_per_gpu": B, "global_batch": B * world, "seq_len": L, "dim": d, "depth": N, "sig_dim": D,
+            "workload": f"{args.config}: B={B_global if scaling == 'strong' else B} L={L} d={d} N={N} fp32 "
+                        "batched truncated signature"
+                        + (" (BASELINE.json configs[1], headline)" if args.config == "c2" else "")
+                        + (f", global batch sharded over {world} GPU(s) (BASELINE.json configs[4])"
+                           if scaling == "strong" else " per GPU"),
+            "batch_per_gpu": B, "global_batch": B_all, "seq_len": L, "dim": d, "depth": N, "sig_dim": D,
             "parallelism": f"batch-sharded x{world}, no collective",
-            "l2": f"inputs rotate over {n_buf} device batches = {n_buf * in_bytes / 2**20:.0f} MiB (> 126 MB L2)",
+            "l2": f"L2 flushed (512 MiB write) before the timed region; every step reads a distinct batch of a "
+                  f"{n_buf}-batch pool ({n_buf * in_bytes / 2**20:.0f} MiB, > 2x the 126 MB L2) so inputs come "
+                  "from HBM",
             "timing": f"{steps} steps = CUDA graph of {S} steps x {reps_full}"
                       + (f" + {rem}" if rem else "") + "; CUDA events on the launch stream; max over ranks",
             "family": sk.FAMILY_NAMES.get(st.family, "?"), "segments": st.segments,
             "chunks": st.chunks, "prefix_len": st.prefix_len, "threads_per_unit": st.threads_per_unit,
             "fold_steps_per_unit": st.fold_steps, "merge_rounds": st.scan_passes,
-            "single_launch_ms": single_ms,
+            "single_launch_ms_eager": single_ms,
             "parity_max_level_rel_err": parity,
         },
         "roofline": {
@@ -428,24 +498,28 @@ def run_ours(args):
                            f"nominal {NOMINAL_FP32_TFLOPS:.2f}",
             "achieved_from": "credited flops per step / mean step interval of the timed back-to-back graph "
                              "replays (CUDA events around the timed region; includes every kernel of the step "
-                             "and the inter-kernel gaps)",
+                             "and the inter-kernel gaps; consecutive launches may overlap via PDL)",
             "kernels_per_step": st.launches,
             "credited_flops_per_launch": B * flops_path,
-            "kernel_ms_event_bracketed": fold_s * 1e3,
-            "kernel_ms_event_bracketed_note": "fold kernel alone, events around every 4th launch of an untimed "
-                                              "replay (no launch overlap)",
+            "single_call": {"kernel_ms": fold_s * 1e3, "achieved": single_tf,
+                            "frac": single_tf / peak if peak else None,
+                            "from": "the fold kernel alone: CUDA events around every 4th launch of an untimed "
+                                    "graph replay after an L2 flush (no launch overlap)"},
             "hbm": {"algorithmic_bytes_per_launch": B * bytes_path,
                     "achieved_gbs": B * bytes_path / (elapsed / steps) / 1e9,
                     "peak_gbs": peaks.get("hbm_gbs"), "peak_source": "MEASURED_PEAKS.json"},
             "traffic": traffic,
         },
         "cpu_baseline": cpu,
-        "e2e": {"value": world * B * e2e_steps / e2e_s, "unit": "paths/s",
-                "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": B * D * 4, "steps": e2e_steps,
+        "e2e": {"value": B_all * e2e_steps / e2e_s, "unit": "paths/s",
+                "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h, "steps": e2e_steps,
                 "api": "sigk_signature_f32 (C ABI), pinned host buffers, SIGK_ASYNC_HOST: every step copies its "
                        "inputs H2D and its signatures D2H; consecutive steps overlap on the copy engines; timed "
                        "to the last result on the host",
-                "synchronous": {"value": world * B * e2e_steps / e2e_sync_s, "unit": "paths/s",
+                "link_gbs": {"h2d": e2e_h2d * e2e_steps / e2e_s / 1e9, "d2h": e2e_d2h * e2e_steps / e2e_s / 1e9,
+                             "note": "per GPU; PCIe bounds e2e at these shapes (the kernel is ~"
+                                     f"{(e2e_s / e2e_steps) / (elapsed / steps):.0f}x faster than the copies)"},
+                "synchronous": {"value": B_all * e2e_steps / e2e_sync_s, "unit": "paths/s",
                                 "api": "same call without SIGK_ASYNC_HOST (returns with each step's result)"}},
         "clocks": clk.summary(),
         "gpu_launches": steps * max(1, st.launches),
@@ -506,15 +580,28 @@ def run_reference(args):
         _, kind = cpu_reference_run(Xs, N, threads)
     dt = time.perf_counter() - t0
     value = rows * args.steps / dt
+    # also 1 thread (as shipped) and the <float> instantiation,
+    # each on a bounded sample (~3 s), reported beside the headline figure
+    var = []
+    for prec, Xv in (("f64", X), ("f32", X.astype(np.float32))):
+        for th in sorted({1, threads}):
+            if prec == "f64" and th == threads:
+                continue
+            vv, r, n, t, k = cpu_timed(Xv[:rows], N, th, 3.0)
+            var.append({"value": vv, "unit": "paths/s", "threads": th, "precision": prec, "kind": k,
+                        "sample": f"{r} rows, best of {n} passes ({t:.1f} s)"})
     line = {
         "metric": baseline_metric(), "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic Brownian paths (numpy, seed 42)",
+        "scaling": rank_rows(args.config, 1, 0)[3], "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic Brownian paths (numpy, seed 42)",
         "impl": "reference",
-        "config": {"workload": f"{args.config}: B={B} L={L} d={d} N={N}", "batch_per_step": rows,
+        "config": {"workload": f"{args.config}: B={B} L={L} d={d} N={N} (CPU, rank 0 only)", "batch_per_step": rows,
                    "seq_len": L, "dim": d, "depth": N},
         "cpu_baseline": {"value": value, "unit": "paths/s", "cores": threads, "kind": kind,
-                         "sample": f"{rows} of {B} rows per step, sigkit_ref::detail::sequential_forward<double>"},
+                         "sample": f"{rows} of {B} rows per step, sigkit_ref::detail::sequential_forward<double>, "
+                                   f"{threads} threads (rows split over std::thread)",
+                         "cpu_model": cpu_model(), "variants": var},
         "e2e": {"value": value, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -1,6 +1,8 @@
 """CPU (gloo, world_size 2): the multi-GPU plumbing — contiguous row shards,
-the all-gather of output rows, max-over-ranks timing — with the CPU oracle
-standing in for the per-rank device call (test infrastructure only)."""
+the all-gather of output rows, max-over-ranks timing, and bench.py's own
+per-rank row split (rank_rows: c5 strong-scaled over shards of the global
+batch) — with the CPU oracle standing in for the per-rank device call (test
+infrastructure only)."""
 import os
 import socket
 
@@ -38,6 +40,47 @@ def _worker(rank, world, port, B, L, d, N, q):
             q.put((full.numpy(), slowest))
     finally:
         dist.destroy_process_group()
+
+
+def _bench_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        from oracle import oracle as O
+
+        B_global, row0, rows, scaling = bench.rank_rows("c5", world, rank)
+        rng = np.random.default_rng(5)
+        X = np.cumsum(rng.standard_normal((B_global, 3, 2)) * 0.3, axis=1)  # c5's batch, tiny paths
+        local = torch.from_numpy(O.signature(X[row0:row0 + rows], 2))
+        full = gather_rows(local, B_global)
+        weak = bench.rank_rows("c2", world, rank)
+        if rank == 0:
+            q.put((full.numpy(), scaling, rows, weak))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_bench_c5_shards():
+    from oracle import oracle as O
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full, scaling, rows, weak = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(5)
+    X = np.cumsum(rng.standard_normal((8192, 3, 2)) * 0.3, axis=1)
+    assert scaling == "strong" and rows == 4096
+    assert np.array_equal(full, O.signature(X, 2))  # the sharded global batch == the single-GPU batch
+    assert weak == (256, 0, 128, "weak")  # c2: every rank folds its own 128 rows
 
 
 @pytest.mark.parametrize("B", [7, 8])
