@@ -134,7 +134,21 @@ typedef struct sigk_tuning {
     int32_t family;         /* SIGK_FAMILY_*: restrict the planner to one family (0: auto) */
     void* phase_buf;        /* optional device buffer of B*8 int64: per-CTA SM-clock
                                timestamps of the path kernel's phases (profiling) */
+    int32_t mode;           /* SIGK_MODE_*: what the fold plan optimises (0: automatic) */
+    int32_t fold_variant;   /* pair family: 0 planned, 1 register-table fold, 2 position-table
+                               fold with a producer warp (sigk_stats.family stays PAIR) */
 } sigk_tuning;
+
+/* sigk_tuning.mode. THROUGHPUT plans for back-to-back calls on a stream (launches
+ * overlap through programmatic dependent launch: per-CTA fixed phases hide behind
+ * other CTAs' folds); LATENCY plans for a call that runs alone (all CTAs start
+ * together: more warps per SM, wide CTAs, thread-block-cluster segment combine).
+ * AUTO = THROUGHPUT for device-buffer calls, LATENCY for synchronous host-buffer
+ * calls. The plan (hence the rounding of the result) is a deterministic function
+ * of the call's arguments and mode. */
+#define SIGK_MODE_AUTO 0
+#define SIGK_MODE_THROUGHPUT 1
+#define SIGK_MODE_LATENCY 2
 
 int sigk_sig_dim(int d, int N, size_t* D);
 int sigk_level_offsets(int d, int N, size_t* offsets /* N+1 entries */);

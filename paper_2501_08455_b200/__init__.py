@@ -62,7 +62,10 @@ class _Tuning(C.Structure):
     _fields_ = [("chunks", C.c_int32), ("force_generic", C.c_int32), ("plan_rows", C.c_int64),
                 ("fold_event_start", C.c_void_p), ("fold_event_stop", C.c_void_p), ("prefix_len", C.c_int32),
                 ("no_overlap", C.c_int32), ("segments", C.c_int32), ("family", C.c_int32),
-                ("phase_buf", C.c_void_p)]
+                ("phase_buf", C.c_void_p), ("mode", C.c_int32), ("fold_variant", C.c_int32)]
+
+
+MODE_AUTO, MODE_THROUGHPUT, MODE_LATENCY = 0, 1, 2  # sigk_tuning.mode (include/sigk.h SIGK_MODE_*)
 
 
 @dataclass
@@ -280,10 +283,11 @@ def _check_out(out, shape, like, *, pinned: bool = False):
 
 
 def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_generic: bool = False,
-         out=None, plan_rows: int = 0, prefix_len: int = 0, segments: int = 0, family: int = 0):
+         out=None, plan_rows: int = 0, prefix_len: int = 0, segments: int = 0, family: int = 0, mode: int = 0,
+         fold_variant: int = 0):
     st = _Stats()
     tun = _Tuning(chunks=chunks, force_generic=int(force_generic), plan_rows=plan_rows, prefix_len=prefix_len,
-                  segments=segments, family=family)
+                  segments=segments, family=family, mode=mode, fold_variant=fold_variant)
     if _is_torch(paths):
         import torch
 
@@ -363,7 +367,8 @@ def _seq_len(paths) -> int:
 
 def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
               stats: KernelStats | None = None, *, chunks: int = 0, out=None, plan_rows: int = 0,
-              prefix_len: int = 0, segments: int = 0, family: int = 0):
+              prefix_len: int = 0, segments: int = 0, family: int = 0, mode: int = MODE_AUTO,
+              fold_variant: int = 0):
     """Reference ``sigkit::signature`` (kernels.cpp:200-206): (B, L, d) -> (B, D).
 
     ``kernel``/``caps`` dispatch like the reference (select_kernel,
@@ -372,12 +377,16 @@ def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: Exe
     Chen fold. ``chunks`` forces the sequence split of the fold (0 = planned);
     ``plan_rows`` plans the split as if the batch had that many rows (results
     are bitwise independent of batch composition at equal chunking);
-    ``segments``/``family``/``prefix_len`` pin the rest of the plan (tests, tuning).
+    ``segments``/``family``/``prefix_len`` pin the rest of the plan (tests, tuning);
+    ``mode`` picks what the plan optimises (MODE_THROUGHPUT: back-to-back calls,
+    MODE_LATENCY: a call that runs alone; MODE_AUTO: latency for numpy inputs,
+    throughput for device tensors); ``fold_variant`` pins the pair family's fold
+    (1 register table, 2 position table with a producer warp; 0 planned).
     """
     if select_kernel(kernel, caps or ExecutionCaps.detect(), _seq_len(paths)) == KernelKind.Parallel:
         return signature_parallel(paths, depth, stats, out=out)
     return _run(paths, depth, stats, chunks=chunks, out=out, plan_rows=plan_rows, prefix_len=prefix_len,
-                segments=segments, family=family)
+                segments=segments, family=family, mode=mode, fold_variant=fold_variant)
 
 
 def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
@@ -580,6 +589,6 @@ __all__ = [
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
     "signature_stream", "signature_vjp", "TrainConfig", "train", "increments", "scaled_increments", "signature_bruteforce",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
-    "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_SCAN", "FAMILY_NAMES", "SIGK_X_ON_DEVICE", "SIGK_OUT_ON_DEVICE",
+    "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_SCAN", "FAMILY_NAMES", "MODE_AUTO", "MODE_THROUGHPUT", "MODE_LATENCY", "SIGK_X_ON_DEVICE", "SIGK_OUT_ON_DEVICE",
     "SIGK_ASYNC_HOST", "SIGK_PREFIX_ROWS", "DEFAULT_PARALLEL_MEMORY_CAP",
 ]

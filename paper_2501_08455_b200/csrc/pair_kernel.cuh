@@ -29,6 +29,8 @@
 //    combine (pair_combine) no longer needs any P_1 ⊗ C cross term.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "fold.cuh"
 
 namespace sigk {
@@ -518,12 +520,21 @@ __device__ __forceinline__ void segment_combine_path(const float* __restrict__ R
     CombineSmem<d, N, P1S> S(smem, G);
     float* top = smem + CLY::floats(G, 0);  // [G][LN] level-N parts of the rows
     const int tid = threadIdx.x, nth = blockDim.x;
-    // stage all G rows at once (every load in flight together; L2 reads)
-    for (int i = tid; i < G * D; i += nth) {
-        const int j = i / D, r = i - (i / D) * D;
-        const float v = __ldcg(Rb + i);
-        if (r < DL) S.ylow[(size_t)j * DL + r] = v;
-        else top[(size_t)j * LN + r - DL] = v;
+    // stage all G rows (L2 reads, 8 loads in flight per thread before the stores)
+    constexpr int V = 8;
+    for (int i0 = tid; i0 < G * D; i0 += V * nth) {
+        float v[V];
+#pragma unroll
+        for (int u = 0; u < V; ++u) v[u] = i0 + u * nth < G * D ? __ldcg(Rb + i0 + u * nth) : 0.f;
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+            const int i = i0 + u * nth;
+            if (i < G * D) {
+                const int j = i / D, r = i - j * D;
+                if (r < DL) S.ylow[(size_t)j * DL + r] = v[u];
+                else top[(size_t)j * LN + r - DL] = v[u];
+            }
+        }
     }
     if (tid < d) S.p10[tid] = 0.f;
     __syncthreads();
@@ -547,6 +558,79 @@ __device__ __forceinline__ void segment_combine_path(const float* __restrict__ R
             acc += x;
         }
         orow[DL + F] = acc;
+    }
+}
+
+// Segment combine inside a thread-block cluster: the G segment CTAs of one
+// path form one cluster, each holds its segment row (A_seg ⊠ C_seg, the same
+// pieces as segment_combine_path) in its own shared memory at `segrow`. Every
+// CTA gathers the G rows over distributed shared memory (no global round
+// trip, no arrival counters), runs the (tiny) scan over the G pieces, and
+// writes its own 1/G share of the output row. Two cluster barriers: rows
+// complete before the gather; gathers complete before any CTA reuses or
+// releases its shared memory.
+template <int d, int N, bool P1S>
+__device__ __forceinline__ void cluster_segment_combine(const float* segrow, int G, float* __restrict__ smem,
+                                                        float* __restrict__ orow) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    using CLY = CombineLayout<d, N>;
+    constexpr int D = level_off(d, N), DL = CLY::DL, LN = CLY::LN;
+    CombineSmem<d, N, P1S> S(smem, G);
+    float* top = smem + CLY::floats(G, 0);  // [G][LN] level-N parts of the rows
+    const int tid = threadIdx.x, nth = blockDim.x;
+    cl.sync();  // every segment row is in its CTA's shared memory
+    constexpr int V = 8;  // remote loads in flight per thread
+    for (int i0 = tid; i0 < G * D; i0 += V * nth) {
+        float v[V];
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+            const int i = i0 + u * nth;
+            v[u] = 0.f;
+            if (i < G * D) {
+                const int j = i / D;
+                v[u] = cl.map_shared_rank(segrow, j)[i - j * D];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+            const int i = i0 + u * nth;
+            if (i < G * D) {
+                const int j = i / D, r = i - j * D;
+                if (r < DL) S.ylow[(size_t)j * DL + r] = v[u];
+                else top[(size_t)j * LN + r - DL] = v[u];
+            }
+        }
+    }
+    if (tid < d) S.p10[tid] = 0.f;
+    cl.sync();  // all gathers done (remote rows may now be released); local staging visible
+    fused_scan<d, N, P1S>(S, G, tid, nth);
+    build_c<d, N, P1S>(S, G, tid, nth);
+    __syncthreads();
+    pdl_wait();  // output writes are ordered after the previous launch
+    const int rank = (int)cl.block_rank();
+    const int per = (D + G - 1) / G, lo = rank * per, hi = min(D, lo + per);
+    const float* pG = S.pf + (size_t)G * DL;
+    for (int i = lo + tid; i < hi; i += nth) {
+        if (i < DL) {
+            orow[i] = pG[i];
+            continue;
+        }
+        const int F = i - DL;
+        float acc = 0.f;
+        for (int j = 0; j < G; ++j) {
+            float x = top[(size_t)j * LN + F];
+            if constexpr (N == 1 && P1S) {
+                if (j != G - 1) x = 0.f;
+            }
+#pragma unroll
+            for (int a = (P1S ? 2 : 1); a < N; ++a) {
+                const int tail = ipow(d, N - a);
+                x = fmaf(S.pf[(size_t)j * DL + level_off(d, a - 1) + F / tail], S.crow(j, N - a)[F % tail], x);
+            }
+            acc += x;
+        }
+        orow[i] = acc;
     }
 }
 
@@ -600,47 +684,26 @@ __device__ __forceinline__ float* pair_stage_and_table(const float* __restrict__
     __syncthreads();
     if (staged_stamp != nullptr && threadIdx.x == 0) *staged_stamp = clock64();  // probes: staging done
     // 2. the operand table: row (s, kk) = (δ_{2kk}[c]/m, δ_{2kk+1}[c]/m), m = 1..NR.
-    //    Column (kk, c) is split into `parts` contiguous step ranges, one per thread;
-    //    steps where both chunks are real run predicate-free, padding steps (δ = 0,
-    //    only in the last chunks of a segment) after them.
+    //    One thread per (step, pair-unit) item, consecutive threads on consecutive
+    //    pair-units of one step (contiguous table rows); every item is independent
+    //    (two points per chunk, no loop-carried dependency), so the loads of a
+    //    thread's items are all in flight together. Steps past a chunk's end
+    //    (only in the last chunks of a segment) get δ = 0.
     {
-        const int cols = UP * d;
-        const int parts = nth / cols > 0 ? nth / cols : 1;
-        const int len = (CL + parts - 1) / parts;
         const int sl = (int)slen;
-        for (int t = tid; t < cols * parts; t += nth) {
-            const int col = t % cols, part = t / cols;
-            const int kk = col / d, c = col - (col / d) * d;
-            const int s0 = part * len, s1 = min(CL, s0 + len);
+        const int items = CL * UP;
+        for (int it = tid; it < items; it += nth) {
+            const int sidx = it / UP, kk = it - (it / UP) * UP;
             const int cs0 = min(2 * kk * CL, sl), cs1 = min((2 * kk + 1) * CL, sl);
-            const int lim0 = min(cs0 + CL, sl) - cs0, lim1 = min(cs1 + CL, sl) - cs1;  // real steps
-            int o0 = (cs0 + s0) * d + c, o1 = (cs1 + s0) * d + c;
-            int ro = (s0 * UP + kk) * RS + c;
-            float x0 = s0 <= lim0 ? raw[o0] : 0.f, x1 = s0 <= lim1 ? raw[o1] : 0.f;
-            const int sf = min(s1, min(lim0, lim1));
-            int sidx = s0;
-#pragma unroll 4
-            for (; sidx < sf; ++sidx) {
-                const float y0 = raw[o0 + d], y1 = raw[o1 + d];
-                const float dl0 = y0 - x0, dl1 = y1 - x1;
-                x0 = y0;
-                x1 = y1;
+            const bool r0 = sidx < min(cs0 + CL, sl) - cs0, r1 = sidx < min(cs1 + CL, sl) - cs1;  // real steps
+            const float* p0 = raw + (cs0 + sidx) * d;
+            const float* p1 = raw + (cs1 + sidx) * d;
+            f2* row = tab + (size_t)it * RS;
 #pragma unroll
-                for (int m = 1; m <= NR; ++m) tab[ro + (m - 1) * RP] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
-                o0 += d;
-                o1 += d;
-                ro += UP * RS;
-            }
-            for (; sidx < s1; ++sidx) {
-                const float y0 = sidx < lim0 ? raw[o0 + d] : x0, y1 = sidx < lim1 ? raw[o1 + d] : x1;
-                const float dl0 = y0 - x0, dl1 = y1 - x1;
-                x0 = y0;
-                x1 = y1;
+            for (int c = 0; c < d; ++c) {
+                const float dl0 = r0 ? p0[d + c] - p0[c] : 0.f, dl1 = r1 ? p1[d + c] - p1[c] : 0.f;
 #pragma unroll
-                for (int m = 1; m <= NR; ++m) tab[ro + (m - 1) * RP] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
-                o0 += d;
-                o1 += d;
-                ro += UP * RS;
+                for (int m = 1; m <= NR; ++m) row[(m - 1) * RP + c] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
             }
         }
     }
@@ -654,7 +717,7 @@ struct PairGeom {
     int U, UP, CL;  // chunks per segment (even), pair-units, steps per chunk
     int threads;    // block size (multiple of 32, >= UP * P)
     int raw_floats; // (SL + 1) * d rounded up to 4
-    long long* phases;  // optional [grid][8] SM-clock stamps of thread 0 (tools/pair_probe.py)
+    long long* phases;  // optional [grid][12] SM-clock stamps of thread 0 (10) + globaltimer at entry/exit (tools/pair_probe.py)
     int* counters;      // G > 1: [B] arrival counters (zero between launches)
     int smem_bytes;     // dynamic shared memory of the launch (the last 16 bytes hold a flag)
     float* final_out;   // G > 1: (B, D) signatures (the kernel's `out` then holds the (B*G, D) segment rows)
@@ -664,23 +727,120 @@ struct PairGeom {
     float* pub = nullptr;
     int* flags = nullptr;
     int epoch = 0;
+    int segrow_off = 0;  // cluster launches: byte offset of the segment row in shared memory
 };
 
+// Offset of the cluster path's segment row (past every other use of the buffer).
 template <int d, int N, int Q>
-__host__ __device__ constexpr size_t pair_smem_bytes(int U, int CL, int raw_floats, int G = 1) {
+__host__ __device__ constexpr size_t pair_segrow_off(int U, int CL, int raw_floats, int G) {
     using PF = PairFold<d, N, Q>;
     const size_t seg = G > 1 ? (CombineLayout<d, N>::floats(G, 0) + (size_t)G * ipow(d, N)) * 4 : 0;
     const size_t fold = (size_t)CL * (U / 2) * PF::RS * 8 + (size_t)raw_floats * 4 + 16 + 16;
     const size_t comb = CombineLayout<d, N>::floats(U, U / 2) * 4;
     const size_t m = fold > comb ? fold : comb;
-    return (m > seg ? m : seg) + 16;  // + the segment-combine flag
+    return ((m > seg ? m : seg) + 15) / 16 * 16;
+}
+
+template <int d, int N, int Q>
+__host__ __device__ constexpr size_t pair_smem_bytes(int U, int CL, int raw_floats, int G = 1, bool cluster = false) {
+    return pair_segrow_off<d, N, Q>(U, CL, raw_floats, G) + (cluster ? (size_t)level_off(d, N) * 4 : 0) +
+           16;  // + the segment-combine flag
+}
+
+// Steps 5-6 of a pair-family CTA after its fold (shared by pair_kernel and
+// ppair_kernel): combine the U chunks of the segment (Chen, tensor_algebra.cpp:
+// 80-102) and write the row, or hand it to the segment combine when G > 1.
+// Every thread of the CTA calls it (fold threads with `active`).
+template <typename PF, bool CLUSTER, bool P1S, typename Phase>
+__device__ __forceinline__ void pair_combine_store(const f2 (&st)[PF::S], bool active, int k, int pre, float p10v,
+                                                   const PairGeom& g, int64_t rowid, int64_t b,
+                                                   float* __restrict__ out, unsigned char* smem_raw, Phase phase) {
+    constexpr int d = PF::d, N = PF::N, Q = PF::QQ, FJ = PF::FJ;
+    using CLY = CombineLayout<d, N>;
+    constexpr int D = level_off(d, N), DL = CLY::DL, LN = CLY::LN;
+    const int U = g.U, UP = g.UP;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    CombineSmem<d, N, P1S> S(reinterpret_cast<float*>(smem_raw), U);
+    if (active) store_low_levels<PF, 1>(st, k, pre, S.ylow);
+    if constexpr (N >= 2) {
+        if (tid < d) S.p10[tid] = p10v;  // P^(0)_1
+    }
+    __syncthreads();
+    fused_scan<d, N, P1S>(S, U, tid, nth);
+    build_c<d, N, P1S>(S, U, tid, nth);
+    __syncthreads();
+    phase(5);
+    float* orow = out + rowid * D;
+    if (active) {
+        constexpr int ot = PF::top_off(N);
+        float r[FJ];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = 2 * k + h;
+            float acc[FJ];
+#pragma unroll
+            for (int J = 0; J < FJ; ++J) {
+                float lo, hi;
+                f2_unpack(st[ot + J], lo, hi);
+                acc[J] = h ? hi : lo;
+                if constexpr (N == 1 && P1S) {
+                    if (j != U - 1) acc[J] = 0.f;  // level 1 of the segment = the last chunk's Y_1
+                }
+            }
+            top_cross_slice<d, N, Q, P1S, P1S ? 2 : 1>(S, j, pre, acc);
+#pragma unroll
+            for (int J = 0; J < FJ; ++J) r[J] = h ? r[J] + acc[J] : acc[J];
+        }
+        float* rr = S.red + (size_t)k * CLY::LNP + (size_t)pre * FJ;
+#pragma unroll
+        for (int J = 0; J < FJ; ++J) rr[J] = r[J];
+    }
+    __syncthreads();
+    phase(6);
+    if constexpr (CLUSTER) {
+        // the segment row stays in shared memory for the cluster combine
+        float* segrow = reinterpret_cast<float*>(smem_raw + g.segrow_off);
+        const float* pU = S.pf + (size_t)U * DL;
+        for (int i = tid; i < DL; i += nth) segrow[i] = pU[i];
+        sum_rows<LN, CLY::LNP>(S.red, UP, segrow + DL);
+        phase(7);
+        phase(8);
+        cluster_segment_combine<d, N, P1S>(segrow, g.G, reinterpret_cast<float*>(smem_raw), out + b * D);
+        phase(9);
+        return;
+    }
+    pdl_wait();  // the previous launch has completed: output writes are ordered after its
+    const float* pU = S.pf + (size_t)U * DL;
+    for (int i = tid; i < DL; i += nth) orow[i] = pU[i];
+    sum_rows<LN, CLY::LNP>(S.red, UP, orow + DL);
+    phase(7);
+    if (g.G > 1) {
+        // segment row written to scratch; the last of the path's G CTAs combines them
+        // (classic fence + counter: no second kernel, no grid-wide serialisation)
+        int* s_last = reinterpret_cast<int*>(smem_raw + g.smem_bytes - 16);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) *s_last = atomicAdd(g.counters + b, 1) == g.G - 1;
+        __syncthreads();
+        phase(8);
+        if (*s_last) {
+            __threadfence();
+            if (tid == 0) g.counters[b] = 0;  // ready for the next launch
+            segment_combine_path<d, N, P1S>(out + b * g.G * D, g.G, reinterpret_cast<float*>(smem_raw),
+                                            g.final_out + b * D);
+        }
+    }
+    phase(9);
 }
 
 // X: (B, L, d) fp32. grid = B * G CTAs; CTA (b, g) folds steps
 // [g*SL, min((g+1)*SL, M)) of path b as U chunks and writes row b*G + g of
 // `out` ((B*G, D)): A_seg ⊠ C_seg with A_seg = (1, X[seg start] - X[0], 0, ...),
 // i.e. the path's signature when G == 1.
-template <int DIM, int DEPTH, int Q, int NT, int MINB, bool P1S = (DIM > 1 && DEPTH > 1)>
+// CLUSTER: launched with a cluster of G CTAs per path (G <= 8); the segment
+// rows are combined over distributed shared memory (cluster_segment_combine)
+// and `out` is the (B, D) output itself.
+template <int DIM, int DEPTH, int Q, int NT, int MINB, bool CLUSTER = false, bool P1S = (DIM > 1 && DEPTH > 1)>
 __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict__ X, int64_t L, PairGeom g,
                                                         float* __restrict__ out) {
     using PF = PairFold<DIM, DEPTH, Q>;
@@ -704,7 +864,14 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
     uint64_t* bar = reinterpret_cast<uint64_t*>(raw + g.raw_floats + 4);         // staging mbarrier
 
     auto phase = [&](int i) {
-        if (g.phases != nullptr && tid == 0) g.phases[rowid * 10 + i] = clock64();
+        if (g.phases != nullptr && tid == 0) {
+            g.phases[rowid * 12 + i] = clock64();
+            if (i == 0 || i == 9) {  // wall time (ns) at entry and exit: SM clock and launch spread
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                g.phases[rowid * 12 + 10 + (i == 9)] = (long long)t;
+            }
+        }
     };
     phase(0);
     pdl_trigger();  // the next launch may start on free SMs now
@@ -721,7 +888,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
     float p10v = 0.f;
     if (P1S && tid < d) p10v = __ldg(xb + seg0 * d + tid) - __ldg(xb + tid);
     raw = pair_stage_and_table<PF>(xb, seg0, slen, CL, UP, tab, raw, bar,
-                                   (g.phases != nullptr && g.G == 1) ? g.phases + rowid * 10 + 8 : nullptr);
+                                   (g.phases != nullptr && g.G == 1) ? g.phases + rowid * 12 + 8 : nullptr);
     phase(1);
     // 3. per-thread state: slice `pre` of chunks 2k and 2k+1, started from (1, X[s_j] - X[0], 0, ...)
     f2 st[PF::S];
@@ -769,65 +936,7 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
     __syncthreads();  // table and staging are dead: reuse them for the combine
     phase(4);
     // 5. combine the U chunks
-    CombineSmem<d, N, P1S> S(reinterpret_cast<float*>(smem_raw), U);
-    if (active) store_low_levels<PF, 1>(st, k, pre, S.ylow);
-    if constexpr (N >= 2) {
-        if (tid < d) S.p10[tid] = p10v;  // P^(0)_1
-    }
-    __syncthreads();
-    fused_scan<d, N, P1S>(S, U, tid, nth);
-    build_c<d, N, P1S>(S, U, tid, nth);
-    __syncthreads();
-    phase(5);
-    float* orow = out + rowid * D;
-    if (active) {
-        constexpr int ot = PF::top_off(N);
-        float r[FJ];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int j = 2 * k + h;
-            float acc[FJ];
-#pragma unroll
-            for (int J = 0; J < FJ; ++J) {
-                float lo, hi;
-                f2_unpack(st[ot + J], lo, hi);
-                acc[J] = h ? hi : lo;
-                if constexpr (N == 1 && P1S) {
-                    if (j != U - 1) acc[J] = 0.f;  // level 1 of the segment = the last chunk's Y_1
-                }
-            }
-            top_cross_slice<d, N, Q, P1S, P1S ? 2 : 1>(S, j, pre, acc);
-#pragma unroll
-            for (int J = 0; J < FJ; ++J) r[J] = h ? r[J] + acc[J] : acc[J];
-        }
-        float* rr = S.red + (size_t)k * CLY::LNP + (size_t)pre * FJ;
-#pragma unroll
-        for (int J = 0; J < FJ; ++J) rr[J] = r[J];
-    }
-    __syncthreads();
-    phase(6);
-    pdl_wait();  // the previous launch has completed: output writes are ordered after its
-    const float* pU = S.pf + (size_t)U * DL;
-    for (int i = tid; i < DL; i += nth) orow[i] = pU[i];
-    sum_rows<LN, CLY::LNP>(S.red, UP, orow + DL);
-    phase(7);
-    if (g.G > 1) {
-        // segment row written to scratch; the last of the path's G CTAs combines them
-        // (classic fence + counter: no second kernel, no grid-wide serialisation)
-        int* s_last = reinterpret_cast<int*>(smem_raw + g.smem_bytes - 16);
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) *s_last = atomicAdd(g.counters + b, 1) == g.G - 1;
-        __syncthreads();
-        phase(8);
-        if (*s_last) {
-            __threadfence();
-            if (tid == 0) g.counters[b] = 0;  // ready for the next launch
-            segment_combine_path<d, N, P1S>(out + b * g.G * D, g.G, reinterpret_cast<float*>(smem_raw),
-                                            g.final_out + b * D);
-        }
-        phase(9);
-    }
+    pair_combine_store<PF, CLUSTER, P1S>(st, active, k, pre, p10v, g, rowid, b, out, smem_raw, phase);
 }
 
 }  // namespace sigk

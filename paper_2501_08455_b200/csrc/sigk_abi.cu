@@ -158,10 +158,41 @@ static double model_pair(const Variant& v, int64_t B, int64_t M, int sms, int G,
     return t;
 }
 
+// Pair family, one call with nothing to overlap (a synchronous call, the
+// first launch on an idle GPU, a training step): every CTA of the launch
+// starts together, so phases do not hide each other. Time = the busiest
+// SM's fold (c CTAs of `warps` warps folding CL steps; FMA-pipe efficiency by
+// warps per SMSP, measured with tools/pair_step_probe.cu: 0.5 / 0.67 / 0.7 /
+// 0.73 at 1 / 2 / 3 / 4) plus the serial phases of one CTA (staging latency,
+// table build, chunk combine, output, the cluster combine when G > 1).
+static double lat_eff(double wps) {
+    if (wps >= 4.0) return 0.73;
+    if (wps >= 3.0) return 0.70 + 0.03 * (wps - 3.0);
+    if (wps >= 2.0) return 0.67 + 0.03 * (wps - 2.0);
+    if (wps >= 1.0) return 0.5 + 0.17 * (wps - 1.0);
+    return 0.5 * wps;
+}
+
+static double model_pair_latency(const Variant& v, int64_t B, int64_t M, int sms, int G, int U, int occ) {
+    const int64_t SL = (M + G - 1) / G;
+    const int64_t CL = (SL + U - 1) / U;
+    const int64_t ctas = B * G;
+    const int warps = (int)((U / 2 * v.P + 31) / 32);
+    const int64_t per_sm = (ctas + sms - 1) / sms;
+    const int64_t c = std::min<int64_t>(per_sm, std::max(1, occ));
+    const int64_t waves = (per_sm + c - 1) / c;
+    const double wps = c * warps / 4.0;
+    const double fold = c * warps * (double)CL * v.ops * 2.0 / 4.0 / lat_eff(wps);
+    const double table = (double)CL * (U / 2) * v.d * 6.0 / (warps * 32.0) * c;
+    const double fixed = 1500.0 + table + 400.0 + 40.0 * U + 800.0 + (G > 1 ? 2500.0 : 0.0);
+    return waves * (fold + fixed);
+}
+
 struct Plan {
     const Variant* v = nullptr;
     int U = 1;
     int G = 1;
+    bool pos = false;  // pair family: position-table fold with a producer warp (ppair_kernel.cuh)
 };
 
 static const int kSegCands[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 14, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 112, 128,
@@ -175,6 +206,8 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
     const int fq = tun ? tun->prefix_len : 0;
     const int fU = tun ? tun->chunks : 0;
     const int fG = tun ? tun->segments : 0;
+    const bool latency = tun && tun->mode == SIGK_MODE_LATENCY;
+    const int fvar = tun ? tun->fold_variant : 0;
     bool have_pair = false;
     for (int k = 0; k < nc; ++k)
         if (cands[k]->family == KernelFamily::Pair && (fam == 0 || fam == SIGK_FAMILY_PAIR) && (fq == 0 || fq == cands[k]->Q))
@@ -216,21 +249,36 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
                 const int G = gl[gi];
                 if (G > 1 && (N < 2 || (fG == 0 && (int64_t)G * 4 > M) || G > M)) continue;
                 const int64_t SL = (M + G - 1) / G;
-                const int umax = std::max(2, 2 * v.pair_units_max);
+                // latency plans may use the wide (512-thread) CTA when no cluster is involved
+                const bool wide_ok = latency && (G == 1 || G > kMaxPairCluster);
+                const int umax = std::max(2, 2 * (wide_ok ? v.pair_units_wide : v.pair_units_max));
                 // a forced chunk count is rounded down to even (>= 2) and clamped to one CTA
                 const int uforce = fU > 0 ? std::min(umax, std::max(2, fU / 2 * 2)) : 0;
                 for (int U = 2; U <= umax; U += 2) {
                     if (uforce > 0 && U != uforce) continue;
                     if (uforce == 0 && U > 2 && U > SL + 1) break;  // whole empty pair-units
                     const int CL = (int)((SL + U - 1) / U);
-                    int occ = 0;
-                    if (v.pair_occupancy(U, CL, SL, G, &occ) != cudaSuccess || occ < 1) continue;
-                    const double t = model_pair(v, B, M, sms, G, U, occ);
-                    if (t < best_t * 0.995) {
-                        best_t = t;
-                        best.v = &v;
-                        best.U = U;
-                        best.G = G;
+                    for (int pos = 0; pos < 2; ++pos) {
+                        // the position-table fold is opt-in (fold_variant = 2): measured on B200 it
+                        // does not beat the register-table fold (profiles/r02/pos_fold_probe.txt)
+                        if (pos && (v.pos_ops == 0 || U / 2 > v.pos_units_max || fvar != 2)) continue;
+                        if (!pos && fvar == 2) continue;
+                        int occ = 0;
+                        if ((pos ? v.pair_pos_occupancy(U, CL, SL, G, &occ) : v.pair_occupancy(U, CL, SL, G, &occ)) !=
+                                cudaSuccess ||
+                            occ < 1)
+                            continue;
+                        Variant vv = v;  // the position-table fold: its op count, no table-build phase
+                        if (pos) vv.ops = v.pos_ops;
+                        double t = latency ? model_pair_latency(vv, B, M, sms, G, U, occ)
+                                           : model_pair(vv, B, M, sms, G, U, occ);
+                        if (t < best_t * 0.995) {
+                            best_t = t;
+                            best.v = &v;
+                            best.U = U;
+                            best.G = G;
+                            best.pos = pos;
+                        }
                     }
                 }
             }
@@ -258,10 +306,10 @@ struct PlanKey {
     int d, N, dev;
     bool f64;
     int64_t B, M;
-    int fam, q, U, G;
+    int fam, q, U, G, mode, fvar;
     bool operator==(const PlanKey& o) const {
         return d == o.d && N == o.N && dev == o.dev && f64 == o.f64 && B == o.B && M == o.M && fam == o.fam &&
-               q == o.q && U == o.U && G == o.G;
+               q == o.q && U == o.U && G == o.G && mode == o.mode && fvar == o.fvar;
     }
 };
 
@@ -269,7 +317,8 @@ static Plan cached_plan(int d, int N, bool is_f64, int dev, int64_t B, int64_t M
     static std::mutex mu;
     static std::vector<std::pair<PlanKey, Plan>> cache;
     const PlanKey key{d, N, dev, is_f64, B, M, tun ? tun->family : 0, tun ? tun->prefix_len : 0,
-                      tun ? tun->chunks : 0, tun ? tun->segments : 0};
+                      tun ? tun->chunks : 0, tun ? tun->segments : 0, tun ? tun->mode : 0,
+                      tun ? tun->fold_variant : 0};
     {
         std::lock_guard<std::mutex> g(mu);
         for (auto& kv : cache)
@@ -444,7 +493,8 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         void* rows = nullptr;
         void* counters = nullptr;
         bool async_rows = false, async_ctr = false;
-        if (G > 1) {
+        const bool cluster = G > 1 && G <= kMaxPairCluster;
+        if (G > 1 && !cluster) {
             if (cap == cudaStreamCaptureStatusNone) cudaStreamIsCapturing(s, &cap);
             const bool capt = cap == cudaStreamCaptureStatusActive;
             rows = segment_scratch(dev, s, 0, sizeof(float) * B * G * D, capt, &async_rows);
@@ -452,7 +502,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
             if (!rows || !counters) return fail(SIGK_ERESOURCE, "segment scratch allocation failed");
         }
         PairLaunch a{X, B, L, G, SL, U, CL, out, rows, counters, s, overlap, ev0, ev1,
-                     cap == cudaStreamCaptureStatusActive, tun ? tun->phase_buf : nullptr};
+                     cap == cudaStreamCaptureStatusActive, tun ? tun->phase_buf : nullptr, cluster, plan.pos};
         e = v->pair_launch(a);
         if (async_rows) cudaFreeAsync(rows, s);
         if (async_ctr) cudaFreeAsync(counters, s);
@@ -740,6 +790,8 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
     cudaStreamWaitEvent(stg.ds, stg.ev[2 * Staging::kPieces], 0);
     sigk_tuning tp = tun ? *tun : sigk_tuning{};
     if (tp.plan_rows <= 0) tp.plan_rows = (int64_t)B;
+    // a synchronous host call has no neighbouring launch to overlap: plan for latency
+    if (tp.mode == SIGK_MODE_AUTO) tp.mode = SIGK_MODE_LATENCY;
     sigk_stats acc{};
     int launches = 0;
     for (int i = 0; i < np && rc == SIGK_OK; ++i) {

@@ -11,6 +11,7 @@
 #include "flat_kernel.cuh"
 #include "ipair_kernel.cuh"
 #include "pair_kernel.cuh"
+#include "ppair_kernel.cuh"
 #include "path_kernel.cuh"
 #include "stream_kernel.cuh"
 #include "variants.h"
@@ -136,11 +137,25 @@ struct PairVariant {
     static constexpr int NT = 256;
     static constexpr int MINB = 2;
     static constexpr auto kernel = pair_kernel<DIM, DEPTH, Q, NT, MINB>;
-    static std::atomic<uint64_t> smem_done;
+    static constexpr auto ckernel = pair_kernel<DIM, DEPTH, Q, NT, MINB, true>;  // cluster segment combine
+    // wide CTAs (latency plans: one path per SM with up to 512 threads, 4 warps per SMSP)
+    static constexpr int NTW = 512;
+    static constexpr auto wkernel = pair_kernel<DIM, DEPTH, Q, NTW, 1>;
+    static std::atomic<uint64_t> smem_done, csmem_done, wsmem_done, psmem_done, pcsmem_done;
+    // position-table fold with a producer warp (ppair_kernel.cuh): Q >= 1, P1S shapes
+    static constexpr bool HAS_POS = Q >= 1 && Q < DEPTH && DIM > 1 && ipow(DIM, Q) <= 128;
+    static constexpr int QP = HAS_POS ? Q : 1;
+    static constexpr int NFP = 128;  // fold threads of a position-table CTA (+ 1 producer warp)
+    static constexpr int TSP = 16;   // steps per table tile
+    static constexpr auto pkernel = ppair_kernel<HAS_POS ? DIM : 2, HAS_POS ? DEPTH : 2, QP, NFP + 32, 3, TSP>;
+    static constexpr auto pckernel = ppair_kernel<HAS_POS ? DIM : 2, HAS_POS ? DEPTH : 2, QP, NFP + 32, 3, TSP, true>;
+    static size_t psmem(int U, int64_t SL, int G, bool cluster) {
+        return ppair_smem_bytes<HAS_POS ? DIM : 2, HAS_POS ? DEPTH : 2, QP>(U, TSP, raw_floats(SL), G, cluster);
+    }
 
     static int raw_floats(int64_t SL) { return (int)(((SL + 1) * DIM + 3) / 4 * 4); }
-    static size_t smem(int U, int CL, int64_t SL, int G) {
-        return pair_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(SL), G);
+    static size_t smem(int U, int CL, int64_t SL, int G, bool cluster = false) {
+        return pair_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(SL), G, cluster);
     }
     static int threads(int U) { return (U / 2 * PF::P + 31) / 32 * 32; }
 
@@ -156,9 +171,55 @@ struct PairVariant {
         g.phases = static_cast<long long*>(a.phases);
         g.counters = static_cast<int*>(a.counters);
         g.final_out = static_cast<float*>(a.out);
-        const size_t sm = smem(a.U, a.CL, a.SL, a.G);
+        const bool cl = a.cluster && a.G > 1;
+        if (a.pos) {  // position-table fold, producer warp
+            if (!HAS_POS || g.threads > NFP) return cudaErrorInvalidValue;
+            const size_t sm = psmem(a.U, a.SL, a.G, cl);
+            g.smem_bytes = (int)sm;
+            g.segrow_off = (int)ppair_segrow_off<HAS_POS ? DIM : 2, HAS_POS ? DEPTH : 2, QP>(a.U, TSP, raw_floats(a.SL), a.G);
+            cudaError_t e = cl ? opt_in_smem(pckernel, sm, pcsmem_done) : opt_in_smem(pkernel, sm, psmem_done);
+            if (e != cudaSuccess) return e;
+            if (a.ev_fold_start) {
+                if (a.capturing) cudaEventRecordWithFlags(static_cast<cudaEvent_t>(a.ev_fold_start), a.s, cudaEventRecordExternal);
+                else cudaEventRecord(static_cast<cudaEvent_t>(a.ev_fold_start), a.s);
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(a.B * a.G));
+            cfg.blockDim = dim3(g.threads + 32);
+            cfg.dynamicSmemBytes = sm;
+            cfg.stream = a.s;
+            cudaLaunchAttribute attr[2];
+            int na = 0;
+            if (cl) {
+                attr[na].id = cudaLaunchAttributeClusterDimension;
+                attr[na].val.clusterDim.x = (unsigned)a.G;
+                attr[na].val.clusterDim.y = 1;
+                attr[na].val.clusterDim.z = 1;
+                ++na;
+            }
+            if (a.overlap && !a.ev_fold_start) {
+                attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[na].val.programmaticStreamSerializationAllowed = 1;
+                ++na;
+            }
+            cfg.attrs = attr;
+            cfg.numAttrs = na;
+            float* dst = static_cast<float*>(a.G > 1 && !cl ? a.scratch : a.out);
+            e = cudaLaunchKernelEx(&cfg, cl ? pckernel : pkernel, static_cast<const float*>(a.X), a.L, g, dst);
+            if (a.ev_fold_stop) {
+                if (a.capturing) cudaEventRecordWithFlags(static_cast<cudaEvent_t>(a.ev_fold_stop), a.s, cudaEventRecordExternal);
+                else cudaEventRecord(static_cast<cudaEvent_t>(a.ev_fold_stop), a.s);
+            }
+            return e;
+        }
+        const bool wide = g.threads > NT;
+        if (wide && (cl || g.threads > NTW)) return cudaErrorInvalidValue;
+        const size_t sm = smem(a.U, a.CL, a.SL, a.G, cl);
         g.smem_bytes = (int)sm;
-        cudaError_t e = opt_in_smem(kernel, sm, smem_done);
+        g.segrow_off = (int)pair_segrow_off<DIM, DEPTH, Q>(a.U, a.CL, raw_floats(a.SL), a.G);
+        cudaError_t e = cl     ? opt_in_smem(ckernel, sm, csmem_done)
+                        : wide ? opt_in_smem(wkernel, sm, wsmem_done)
+                               : opt_in_smem(kernel, sm, smem_done);
         if (e != cudaSuccess) return e;
         auto record = [&](void* ev) {
             if (!ev) return;
@@ -166,19 +227,53 @@ struct PairVariant {
             else cudaEventRecord(static_cast<cudaEvent_t>(ev), a.s);
         };
         record(a.ev_fold_start);
-        float* dst = static_cast<float*>(a.G > 1 ? a.scratch : a.out);
-        e = launch_maybe_overlapped(kernel, dim3((unsigned)(a.B * a.G)), dim3(g.threads), sm, a.s,
-                                    a.overlap && !a.ev_fold_start, static_cast<const float*>(a.X), a.L, g, dst);
+        if (cl) {  // the path's G segment CTAs form one cluster
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(a.B * a.G));
+            cfg.blockDim = dim3(g.threads);
+            cfg.dynamicSmemBytes = sm;
+            cfg.stream = a.s;
+            cudaLaunchAttribute attr[2];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)a.G;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[1].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = (a.overlap && !a.ev_fold_start) ? 2 : 1;
+            e = cudaLaunchKernelEx(&cfg, ckernel, static_cast<const float*>(a.X), a.L, g, static_cast<float*>(a.out));
+        } else {
+            float* dst = static_cast<float*>(a.G > 1 ? a.scratch : a.out);
+            e = launch_maybe_overlapped(wide ? wkernel : kernel, dim3((unsigned)(a.B * a.G)), dim3(g.threads), sm,
+                                        a.s, a.overlap && !a.ev_fold_start, static_cast<const float*>(a.X), a.L, g,
+                                        dst);
+        }
         record(a.ev_fold_stop);
         return e;
     }
-    static cudaError_t occupancy(int U, int CL, int64_t SL, int G, int* blocks) {
-        const size_t sm = smem(U, CL, SL, G);
+    static cudaError_t pos_occupancy(int U, int CL, int64_t SL, int G, int* blocks) {
+        (void)CL;
+        const bool cl = G > 1 && G <= kMaxPairCluster;
+        const size_t sm = psmem(U, SL, G, cl);
         *blocks = 0;
-        if (sm > 227 * 1024) return cudaSuccess;
-        cudaError_t e = opt_in_smem(kernel, sm, smem_done);
+        if (!HAS_POS || sm > 227 * 1024 || threads(U) > NFP) return cudaSuccess;
+        cudaError_t e = cl ? opt_in_smem(pckernel, sm, pcsmem_done) : opt_in_smem(pkernel, sm, psmem_done);
         if (e != cudaSuccess) return e;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kernel, threads(U), sm);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, cl ? pckernel : pkernel, threads(U) + 32, sm);
+    }
+    static cudaError_t occupancy(int U, int CL, int64_t SL, int G, int* blocks) {
+        const bool cl = G > 1 && G <= kMaxPairCluster;
+        const bool wide = threads(U) > NT;
+        const size_t sm = smem(U, CL, SL, G, cl);
+        *blocks = 0;
+        if (sm > 227 * 1024 || threads(U) > NTW || (wide && cl)) return cudaSuccess;
+        cudaError_t e = cl     ? opt_in_smem(ckernel, sm, csmem_done)
+                        : wide ? opt_in_smem(wkernel, sm, wsmem_done)
+                               : opt_in_smem(kernel, sm, smem_done);
+        if (e != cudaSuccess) return e;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, cl ? ckernel : wide ? wkernel : kernel,
+                                                             threads(U), sm);
     }
 
     // prefix stream: one CTA per path; the largest stage tile TS in {8, 4, 2, 1} that fits
@@ -218,6 +313,14 @@ struct PairVariant {
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::smem_done{0};
 template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::csmem_done{0};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::wsmem_done{0};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::psmem_done{0};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::pcsmem_done{0};
+template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::ssmem_done{0};
 
 // Smallest Q whose pair state (two chunks) fits ~80 registers, or -1.
@@ -237,10 +340,16 @@ Variant make_pair_variant() {
     int chen = 0;
     for (int n = 2; n <= DEPTH; ++n) chen += (n - 2) * ipow(DIM, n);
     Variant v{DIM, DEPTH, Q, PF::P, PF::ops_per_step(), PF::loads_per_step(), chen, KernelFamily::Pair, V::NT, 0,
-              nullptr, nullptr, nullptr, nullptr, 0, nullptr};
+              nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, 0, 0, nullptr};
     v.pair_launch = &V::launch;
     v.pair_occupancy = &V::occupancy;
     v.pair_units_max = V::NT / PF::P;
+    v.pair_units_wide = V::NTW / PF::P;
+    if constexpr (V::HAS_POS) {
+        v.pos_ops = PosFold<DIM, DEPTH, V::QP>::ops_per_step();
+        v.pos_units_max = V::NFP / PF::P;
+        v.pair_pos_occupancy = &V::pos_occupancy;
+    }
     v.stream_launch = &V::stream_launch;
     return v;
 }
@@ -293,7 +402,7 @@ Variant make_ipair_variant() {
     using V = IPairVariant<DIM, DEPTH, Q>;
     using F = typename V::F;
     Variant v{DIM, DEPTH, Q, F::P, F::pipe_cycles(), 0, 0, KernelFamily::PFlat, V::NT, V::T,
-              &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr};
+              &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0};
     return v;
 }
 
@@ -306,11 +415,11 @@ Variant make_variant() {
     if constexpr (SF::P > 256) {
         using V = FlatVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Flat, V::NT, V::T,
-                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0};
     } else {
         using V = PathVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Path, V::NTMAX, V::T,
-                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0};
     }
 }
 

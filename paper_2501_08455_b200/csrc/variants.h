@@ -9,10 +9,17 @@ namespace sigk {
 
 enum class KernelFamily : int { Path = 1, Flat = 2, Pair = 3, PFlat = 5 };  // = SIGK_FAMILY_*
 
+// Pair family: segment counts 2..kMaxPairCluster run as thread-block clusters
+// (one cluster per path, segment rows combined over distributed shared memory);
+// larger G combines through global scratch and arrival counters.
+constexpr int kMaxPairCluster = 8;
+
 // One launch of the pair family (pair_kernel.cuh): B*G CTAs of one path
-// segment each (SL steps as U chunks of CL). When G > 1 the segment rows go
-// to `scratch` ((B*G, D) floats) and the last segment CTA of each path (per
-// the zero-initialised `counters`, [B] ints) combines them into `out`.
+// segment each (SL steps as U chunks of CL). When G > 1 and `cluster`, the G
+// CTAs of a path form a cluster and combine their rows over distributed shared
+// memory; otherwise the segment rows go to `scratch` ((B*G, D) floats) and the
+// last segment CTA of each path (per the zero-initialised `counters`, [B]
+// ints) combines them into `out`.
 struct PairLaunch {
     const void* X;
     int64_t B, L;
@@ -28,6 +35,8 @@ struct PairLaunch {
     void* ev_fold_stop;
     bool capturing;
     void* phases;  // optional [B*G][8] int64 phase stamps
+    bool cluster;  // G in [2, kMaxPairCluster]: cluster launch (no scratch, no counters)
+    bool pos;      // position-table fold with a producer warp (ppair_kernel.cuh); U/2 * P <= 128
 };
 
 struct Variant {
@@ -54,6 +63,10 @@ struct Variant {
     // segment does not fit one CTA
     cudaError_t (*stream_launch)(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, bool overlap,
                                  int G, void* pub, int* flags, int epoch);
+    int pair_units_wide;  // pair family: max U/2 of the wide (512-thread) fold CTA, G = 1 or G > kMaxPairCluster
+    int pos_ops;          // pair family: FFMA-pipe ops per thread-step of the position-table fold (0: none)
+    int pos_units_max;    // max U/2 of a position-table CTA
+    cudaError_t (*pair_pos_occupancy)(int U, int CL, int64_t SL, int G, int* blocks_per_sm);
 };
 
 const Variant* find_variant(int d, int N, bool is_f64);  // first (smallest-Q) candidate

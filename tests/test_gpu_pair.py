@@ -166,3 +166,34 @@ def test_pflat_c5_rows(sk):
     for lo in (0, 500, 1000 - 40):
         errs = level_errors(got[lo:lo + 40], oracle32(X[lo:lo + 40], 4), 8, 4)
         assert max(errs) <= F32_TOL, (lo, errs)
+
+
+# ---- the position-table fold with a producer warp (ppair_kernel.cuh)
+@pytest.mark.parametrize("d,N", [(3, 4), (4, 4), (5, 3), (5, 4), (6, 3), (8, 3)])
+def test_position_table_fold_shapes(sk, d, N):
+    X = brownian(9, 301, d, seed=d * 10 + N)
+    ref = oracle32(X, N)
+    try:
+        got, st = pair(sk, X, N, fold_variant=2)
+    except sk.DeviceError:
+        pytest.skip("no position-table instantiation for this shape")
+    assert max(level_errors(got, ref, d, N)) <= F32_TOL, (d, N)
+
+
+@pytest.mark.parametrize("U,G,L", [(2, 1, 1000), (4, 1, 997), (10, 1, 1000), (6, 1, 37), (10, 2, 1000),
+                                   (8, 4, 2001), (10, 12, 10000), (10, 1, 2)])
+def test_position_table_fold_plans(sk, U, G, L):
+    # ragged chunk ends (empty / partial tiles), cluster and global segment combines
+    X = brownian(7, L, 5, seed=U * 100 + G)
+    ref = oracle32(X, 4)
+    got, st = pair(sk, X, 4, fold_variant=2, chunks=U, segments=G)
+    assert max(level_errors(got, ref, 5, 4)) <= F32_TOL, (U, G, L)
+
+
+def test_position_table_fold_headline_and_batch_invariance(sk):
+    X = brownian(128, 1000, 5, seed=77)
+    ref = oracle32(X, 4)
+    got, _ = pair(sk, X, 4, fold_variant=2, chunks=10, segments=1)
+    assert max(level_errors(got, ref, 5, 4)) <= F32_TOL
+    one, _ = pair(sk, X[5:6], 4, fold_variant=2, chunks=10, segments=1)
+    assert np.array_equal(one[0], got[5])

@@ -31,9 +31,9 @@ for combo in combos:
     kw = {}
     for kv in combo.split(","):
         k, v = kv.split("=")
-        kw[{"U": "chunks", "G": "segments", "Q": "prefix_len"}[k]] = int(v)
+        kw[{"U": "chunks", "G": "segments", "Q": "prefix_len", "M": "mode", "V": "fold_variant"}[k]] = int(v)
     plan = sk.plan(B, L, d, N, family=3, **kw)
-    ph = torch.zeros((B * plan.segments, 10), dtype=torch.int64, device="cuda")
+    ph = torch.zeros((B * plan.segments, 12), dtype=torch.int64, device="cuda")
     res = []
     for it in range(5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -56,16 +56,24 @@ for combo in combos:
         torch.cuda.synchronize()
         res.append(e0.elapsed_time(e1) * 1e3 / (40 if pipelined else 1))
     p = ph.cpu()
+    wall = p[:, 10:12].double()  # globaltimer ns at entry / exit
+    cyc = (p[:, 9] - p[:, 0]).double()
+    mhz = float((cyc / (wall[:, 1] - wall[:, 0]).clamp(min=1)).median().item() * 1e3)
     staged = None
     if plan.segments == 1:  # slot 8 holds the end of staging (inside the stage phase)
         staged = int((p[:, 8] - p[:, 0]).double().median().item())
         p[:, 8] = p[:, 7]
-        p[:, 9] = p[:, 7]
+    if kw.get("fold_variant") == 2:  # ppair: 1 = first tile ready, 2 = producer done (its own clock), 3 = fold done
+        names2 = {"first_tile": p[:, 1] - p[:, 0], "producer_done": p[:, 2] - p[:, 0], "fold_done": p[:, 3] - p[:, 0]}
+        print(json.dumps({k: int(v.double().median().item()) for k, v in names2.items()}), flush=True)
+        p[:, 2] = p[:, 1]
     dlt = (p[:, 1:10] - p[:, 0:9]).double().median(dim=0).values.tolist()
-    start = p[:, 0].double()
+    t0 = wall[:, 0].min()
     rec = {"cfg": name, "B": B, "L": L, "G": st.segments, "U": st.chunks, "CL": st.fold_steps,
            "kernel_us": round(min(res), 2), "phase_cycles": dict(zip(names, [int(x) for x in dlt])),
-           "total_cycles": int((p[:, 9] - p[:, 0]).double().median().item()),
-           "seg_combine_max": int((p[:, 9] - p[:, 8]).max().item()), "staging_done_at": staged,
-           "start_spread_cycles": int((start.max() - start.min()).item())}
+           "total_cycles": int(cyc.median().item()), "sm_mhz": round(mhz),
+           "cta_us_median": round(float((wall[:, 1] - wall[:, 0]).median().item()) / 1e3, 2),
+           "first_to_last_exit_us": round(float((wall[:, 1].max() - t0).item()) / 1e3, 2),
+           "start_spread_us": round(float((wall[:, 0].max() - t0).item()) / 1e3, 2),
+           "staging_done_at": staged}
     print(json.dumps(rec), flush=True)
