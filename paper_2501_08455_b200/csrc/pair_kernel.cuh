@@ -684,26 +684,47 @@ __device__ __forceinline__ float* pair_stage_and_table(const float* __restrict__
     __syncthreads();
     if (staged_stamp != nullptr && threadIdx.x == 0) *staged_stamp = clock64();  // probes: staging done
     // 2. the operand table: row (s, kk) = (δ_{2kk}[c]/m, δ_{2kk+1}[c]/m), m = 1..NR.
-    //    One thread per (step, pair-unit) item, consecutive threads on consecutive
-    //    pair-units of one step (contiguous table rows); every item is independent
-    //    (two points per chunk, no loop-carried dependency), so the loads of a
-    //    thread's items are all in flight together. Steps past a chunk's end
-    //    (only in the last chunks of a segment) get δ = 0.
+    //    Column (kk, c) is split into `parts` contiguous step ranges, one per thread;
+    //    steps where both chunks are real run predicate-free, padding steps (δ = 0,
+    //    only in the last chunks of a segment) after them.
     {
+        const int cols = UP * d;
+        const int parts = nth / cols > 0 ? nth / cols : 1;
+        const int len = (CL + parts - 1) / parts;
         const int sl = (int)slen;
-        const int items = CL * UP;
-        for (int it = tid; it < items; it += nth) {
-            const int sidx = it / UP, kk = it - (it / UP) * UP;
+        for (int t = tid; t < cols * parts; t += nth) {
+            const int col = t % cols, part = t / cols;
+            const int kk = col / d, c = col - (col / d) * d;
+            const int s0 = part * len, s1 = min(CL, s0 + len);
             const int cs0 = min(2 * kk * CL, sl), cs1 = min((2 * kk + 1) * CL, sl);
-            const bool r0 = sidx < min(cs0 + CL, sl) - cs0, r1 = sidx < min(cs1 + CL, sl) - cs1;  // real steps
-            const float* p0 = raw + (cs0 + sidx) * d;
-            const float* p1 = raw + (cs1 + sidx) * d;
-            f2* row = tab + (size_t)it * RS;
+            const int lim0 = min(cs0 + CL, sl) - cs0, lim1 = min(cs1 + CL, sl) - cs1;  // real steps
+            int o0 = (cs0 + s0) * d + c, o1 = (cs1 + s0) * d + c;
+            int ro = (s0 * UP + kk) * RS + c;
+            float x0 = s0 <= lim0 ? raw[o0] : 0.f, x1 = s0 <= lim1 ? raw[o1] : 0.f;
+            const int sf = min(s1, min(lim0, lim1));
+            int sidx = s0;
+#pragma unroll 4
+            for (; sidx < sf; ++sidx) {
+                const float y0 = raw[o0 + d], y1 = raw[o1 + d];
+                const float dl0 = y0 - x0, dl1 = y1 - x1;
+                x0 = y0;
+                x1 = y1;
 #pragma unroll
-            for (int c = 0; c < d; ++c) {
-                const float dl0 = r0 ? p0[d + c] - p0[c] : 0.f, dl1 = r1 ? p1[d + c] - p1[c] : 0.f;
+                for (int m = 1; m <= NR; ++m) tab[ro + (m - 1) * RP] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
+                o0 += d;
+                o1 += d;
+                ro += UP * RS;
+            }
+            for (; sidx < s1; ++sidx) {
+                const float y0 = sidx < lim0 ? raw[o0 + d] : x0, y1 = sidx < lim1 ? raw[o1 + d] : x1;
+                const float dl0 = y0 - x0, dl1 = y1 - x1;
+                x0 = y0;
+                x1 = y1;
 #pragma unroll
-                for (int m = 1; m <= NR; ++m) row[(m - 1) * RP + c] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
+                for (int m = 1; m <= NR; ++m) tab[ro + (m - 1) * RP] = f2_pack(dl0 * (1.0f / m), dl1 * (1.0f / m));
+                o0 += d;
+                o1 += d;
+                ro += UP * RS;
             }
         }
     }

@@ -184,7 +184,7 @@ static double model_pair_latency(const Variant& v, int64_t B, int64_t M, int sms
     const double wps = c * warps / 4.0;
     const double fold = c * warps * (double)CL * v.ops * 2.0 / 4.0 / lat_eff(wps);
     const double table = (double)CL * (U / 2) * v.d * 6.0 / (warps * 32.0) * c;
-    const double fixed = 1500.0 + table + 400.0 + 40.0 * U + 800.0 + (G > 1 ? 2500.0 : 0.0);
+    const double fixed = 1500.0 + table + 400.0 + 40.0 * U + 800.0 + (G > 1 ? 6000.0 : 0.0);  // cluster sync + combine: measured
     return waves * (fold + fixed);
 }
 
@@ -249,9 +249,7 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
                 const int G = gl[gi];
                 if (G > 1 && (N < 2 || (fG == 0 && (int64_t)G * 4 > M) || G > M)) continue;
                 const int64_t SL = (M + G - 1) / G;
-                // latency plans may use the wide (512-thread) CTA when no cluster is involved
-                const bool wide_ok = latency && (G == 1 || G > kMaxPairCluster);
-                const int umax = std::max(2, 2 * (wide_ok ? v.pair_units_wide : v.pair_units_max));
+                const int umax = std::max(2, 2 * v.pair_units_max);
                 // a forced chunk count is rounded down to even (>= 2) and clamped to one CTA
                 const int uforce = fU > 0 ? std::min(umax, std::max(2, fU / 2 * 2)) : 0;
                 for (int U = 2; U <= umax; U += 2) {

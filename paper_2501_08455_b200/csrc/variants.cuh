@@ -138,10 +138,7 @@ struct PairVariant {
     static constexpr int MINB = 2;
     static constexpr auto kernel = pair_kernel<DIM, DEPTH, Q, NT, MINB>;
     static constexpr auto ckernel = pair_kernel<DIM, DEPTH, Q, NT, MINB, true>;  // cluster segment combine
-    // wide CTAs (latency plans: one path per SM with up to 512 threads, 4 warps per SMSP)
-    static constexpr int NTW = 512;
-    static constexpr auto wkernel = pair_kernel<DIM, DEPTH, Q, NTW, 1>;
-    static std::atomic<uint64_t> smem_done, csmem_done, wsmem_done, psmem_done, pcsmem_done;
+    static std::atomic<uint64_t> smem_done, csmem_done, psmem_done, pcsmem_done;
     // position-table fold with a producer warp (ppair_kernel.cuh): Q >= 1, P1S shapes
     static constexpr bool HAS_POS = Q >= 1 && Q < DEPTH && DIM > 1 && ipow(DIM, Q) <= 128;
     static constexpr int QP = HAS_POS ? Q : 1;
@@ -212,14 +209,11 @@ struct PairVariant {
             }
             return e;
         }
-        const bool wide = g.threads > NT;
-        if (wide && (cl || g.threads > NTW)) return cudaErrorInvalidValue;
+        if (g.threads > NT) return cudaErrorInvalidValue;
         const size_t sm = smem(a.U, a.CL, a.SL, a.G, cl);
         g.smem_bytes = (int)sm;
         g.segrow_off = (int)pair_segrow_off<DIM, DEPTH, Q>(a.U, a.CL, raw_floats(a.SL), a.G);
-        cudaError_t e = cl     ? opt_in_smem(ckernel, sm, csmem_done)
-                        : wide ? opt_in_smem(wkernel, sm, wsmem_done)
-                               : opt_in_smem(kernel, sm, smem_done);
+        cudaError_t e = cl ? opt_in_smem(ckernel, sm, csmem_done) : opt_in_smem(kernel, sm, smem_done);
         if (e != cudaSuccess) return e;
         auto record = [&](void* ev) {
             if (!ev) return;
@@ -245,9 +239,8 @@ struct PairVariant {
             e = cudaLaunchKernelEx(&cfg, ckernel, static_cast<const float*>(a.X), a.L, g, static_cast<float*>(a.out));
         } else {
             float* dst = static_cast<float*>(a.G > 1 ? a.scratch : a.out);
-            e = launch_maybe_overlapped(wide ? wkernel : kernel, dim3((unsigned)(a.B * a.G)), dim3(g.threads), sm,
-                                        a.s, a.overlap && !a.ev_fold_start, static_cast<const float*>(a.X), a.L, g,
-                                        dst);
+            e = launch_maybe_overlapped(kernel, dim3((unsigned)(a.B * a.G)), dim3(g.threads), sm, a.s,
+                                        a.overlap && !a.ev_fold_start, static_cast<const float*>(a.X), a.L, g, dst);
         }
         record(a.ev_fold_stop);
         return e;
@@ -264,16 +257,12 @@ struct PairVariant {
     }
     static cudaError_t occupancy(int U, int CL, int64_t SL, int G, int* blocks) {
         const bool cl = G > 1 && G <= kMaxPairCluster;
-        const bool wide = threads(U) > NT;
         const size_t sm = smem(U, CL, SL, G, cl);
         *blocks = 0;
-        if (sm > 227 * 1024 || threads(U) > NTW || (wide && cl)) return cudaSuccess;
-        cudaError_t e = cl     ? opt_in_smem(ckernel, sm, csmem_done)
-                        : wide ? opt_in_smem(wkernel, sm, wsmem_done)
-                               : opt_in_smem(kernel, sm, smem_done);
+        if (sm > 227 * 1024 || threads(U) > NT) return cudaSuccess;
+        cudaError_t e = cl ? opt_in_smem(ckernel, sm, csmem_done) : opt_in_smem(kernel, sm, smem_done);
         if (e != cudaSuccess) return e;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, cl ? ckernel : wide ? wkernel : kernel,
-                                                             threads(U), sm);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, cl ? ckernel : kernel, threads(U), sm);
     }
 
     // prefix stream: one CTA per path; the largest stage tile TS in {8, 4, 2, 1} that fits
@@ -315,8 +304,6 @@ std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::smem_done{0};
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::csmem_done{0};
 template <int DIM, int DEPTH, int Q>
-std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::wsmem_done{0};
-template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::psmem_done{0};
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::pcsmem_done{0};
@@ -340,11 +327,10 @@ Variant make_pair_variant() {
     int chen = 0;
     for (int n = 2; n <= DEPTH; ++n) chen += (n - 2) * ipow(DIM, n);
     Variant v{DIM, DEPTH, Q, PF::P, PF::ops_per_step(), PF::loads_per_step(), chen, KernelFamily::Pair, V::NT, 0,
-              nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, 0, 0, nullptr};
+              nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, 0, nullptr};
     v.pair_launch = &V::launch;
     v.pair_occupancy = &V::occupancy;
     v.pair_units_max = V::NT / PF::P;
-    v.pair_units_wide = V::NTW / PF::P;
     if constexpr (V::HAS_POS) {
         v.pos_ops = PosFold<DIM, DEPTH, V::QP>::ops_per_step();
         v.pos_units_max = V::NFP / PF::P;
@@ -402,7 +388,7 @@ Variant make_ipair_variant() {
     using V = IPairVariant<DIM, DEPTH, Q>;
     using F = typename V::F;
     Variant v{DIM, DEPTH, Q, F::P, F::pipe_cycles(), 0, 0, KernelFamily::PFlat, V::NT, V::T,
-              &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0};
+              &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr};
     return v;
 }
 
@@ -415,11 +401,11 @@ Variant make_variant() {
     if constexpr (SF::P > 256) {
         using V = FlatVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Flat, V::NT, V::T,
-                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr};
     } else {
         using V = PathVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Path, V::NTMAX, V::T,
-                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr};
     }
 }
 

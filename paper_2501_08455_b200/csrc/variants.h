@@ -63,7 +63,6 @@ struct Variant {
     // segment does not fit one CTA
     cudaError_t (*stream_launch)(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s, bool overlap,
                                  int G, void* pub, int* flags, int epoch);
-    int pair_units_wide;  // pair family: max U/2 of the wide (512-thread) fold CTA, G = 1 or G > kMaxPairCluster
     int pos_ops;          // pair family: FFMA-pipe ops per thread-step of the position-table fold (0: none)
     int pos_units_max;    // max U/2 of a position-table CTA
     cudaError_t (*pair_pos_occupancy)(int U, int CL, int64_t SL, int G, int* blocks_per_sm);

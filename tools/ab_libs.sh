@@ -6,7 +6,7 @@ for rep in 1 2; do
 for lib in "$@"; do
   for shp in $shapes; do
     arg=""; [ "$shp" != "c2" ] && arg="--shape $shp"
-    SIGK_LIB_PATH=paper_2501_08455_b200/$lib.so timeout 300 python bench.py --steps 200 --warmup 5 $arg 2>/dev/null | python -c "
+    SIGK_LIB_PATH=paper_2501_08455_b200/$lib.so timeout 300 python bench.py --steps ${STEPS:-2000} --warmup 20 --no-cpu $arg 2>/dev/null | python -c "
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
