@@ -327,7 +327,7 @@ def run_ours(args):
     S = min(args.steps, GRAPH_STEPS)
     step_events = []
 
-    def capture(nsteps, with_events):
+    def capture(nsteps, with_events, mode=0):
         g = torch.cuda.CUDAGraph()
         evs = {}
         if with_events:  # create the CUDA events (torch creates them lazily on first record)
@@ -338,7 +338,7 @@ def run_ours(args):
             stream.synchronize()
         with torch.cuda.graph(g, stream=stream):
             for j in range(nsteps):
-                _step(sk, pool[j % n_buf], N, out, evs.get(j))
+                _step(sk, pool[j % n_buf], N, out, evs.get(j), mode)
         return g, list(evs.values())
 
     # warm-up (eager + one graph replay)
@@ -350,6 +350,11 @@ def run_ours(args):
     g_main = capture(S, False)[0]  # the timed graph carries no events (they would serialise launches)
     g_rem = capture(rem, False)[0] if rem else None
     g_ev, ev_main = capture(S, True)  # kernel durations, replayed outside the timed region
+    lat_plan = sk.plan(B, L, d, N, mode=sk.MODE_LATENCY, **{k: v for k, v in TUNE.items() if k != "mode"})
+    with torch.cuda.stream(stream):
+        _step(sk, pool[0], N, out, None, sk.MODE_LATENCY)  # plan + scratch outside the capture
+    stream.synchronize()
+    g_lat, ev_lat = capture(min(S, 64), True, sk.MODE_LATENCY)  # the latency plan, same bracketing
     for _ in range(max(1, args.warmup // S)):
         g_main.replay()
     torch.cuda.synchronize()
@@ -377,6 +382,12 @@ def run_ours(args):
     stream.synchronize()
     fold_ms = [a.elapsed_time(b) for a, b in ev_main]
     fold_s = max_over_ranks(sum(fold_ms) / len(fold_ms) * 1e-3, world)
+    with torch.cuda.stream(stream):
+        flush.fill_(3.0)
+        g_lat.replay()
+    stream.synchronize()
+    lat_ms = [a.elapsed_time(b) for a, b in ev_lat]
+    lat_s = max_over_ranks(sum(lat_ms) / len(lat_ms) * 1e-3, world)
 
     # single-launch (non-graph) latency of one step, for reference
     with torch.cuda.stream(stream):
@@ -504,7 +515,14 @@ def run_ours(args):
             "single_call": {"kernel_ms": fold_s * 1e3, "achieved": single_tf,
                             "frac": single_tf / peak if peak else None,
                             "from": "the fold kernel alone: CUDA events around every 4th launch of an untimed "
-                                    "graph replay after an L2 flush (no launch overlap)"},
+                                    "graph replay after an L2 flush (no launch overlap); includes the launch "
+                                    "latency of an idle GPU (a ~1 us C1 fold measures ~8 us this way, "
+                                    "profiles/r02/mode_probe.txt)",
+                            "latency_plan": {"kernel_ms": lat_s * 1e3,
+                                             "frac": B * flops_path / lat_s / 1e12 / peak if peak else None,
+                                             "chunks": lat_plan.chunks, "segments": lat_plan.segments,
+                                             "mode": "sigk_tuning.mode = SIGK_MODE_LATENCY (the plan synchronous "
+                                                     "host calls use)"}},
             "hbm": {"algorithmic_bytes_per_launch": B * bytes_path,
                     "achieved_gbs": B * bytes_path / (elapsed / steps) / 1e9,
                     "peak_gbs": peaks.get("hbm_gbs"), "peak_source": "MEASURED_PEAKS.json"},
@@ -527,12 +545,14 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
-def _step(sk, X, N, out, ev):
+def _step(sk, X, N, out, ev, mode=0):
     import ctypes as C
 
     import torch
 
     tun = sk._Tuning(**TUNE)
+    if mode:
+        tun.mode = mode
     if ev is not None:
         tun.fold_event_start = C.c_void_p(ev[0].cuda_event)
         tun.fold_event_stop = C.c_void_p(ev[1].cuda_event)
