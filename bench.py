@@ -403,10 +403,12 @@ def run_ours(args):
     outh = torch.empty((B, D), dtype=torch.float32).pin_memory()
     lib = sk.lib()
     tun = sk._Tuning(**TUNE)
-    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    # the host-buffer leg runs its own fixed number of steps (the copy ring reaches
+    # steady state only after a few calls); it does not depend on --steps
+    e2e_steps = max(3, args.e2e_steps)
 
     def e2e_time(flags):
-        for _ in range(3):
+        for _ in range(8):
             sk._check(lib.sigk_signature_f32(Xh.data_ptr(), B, L, d, N, outh.data_ptr(), flags,
                                              C.c_void_p(stream.cuda_stream), C.byref(tun), None))
         stream.synchronize()
