@@ -262,7 +262,8 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
                         if (pos && (v.pos_ops == 0 || U / 2 > v.pos_units_max || fvar != 2)) continue;
                         if (!pos && fvar == 2) continue;
                         int occ = 0;
-                        if ((pos ? v.pair_pos_occupancy(U, CL, SL, G, &occ) : v.pair_occupancy(U, CL, SL, G, &occ)) !=
+                        if ((pos ? v.pair_pos_occupancy(U, CL, SL, G, latency, &occ)
+                                 : v.pair_occupancy(U, CL, SL, G, latency, &occ)) !=
                                 cudaSuccess ||
                             occ < 1)
                             continue;
@@ -491,7 +492,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         void* rows = nullptr;
         void* counters = nullptr;
         bool async_rows = false, async_ctr = false;
-        const bool cluster = G > 1 && G <= kMaxPairCluster;
+        const bool cluster = G > 1 && G <= kMaxPairCluster && tun && tun->mode == SIGK_MODE_LATENCY;
         if (G > 1 && !cluster) {
             if (cap == cudaStreamCaptureStatusNone) cudaStreamIsCapturing(s, &cap);
             const bool capt = cap == cudaStreamCaptureStatusActive;

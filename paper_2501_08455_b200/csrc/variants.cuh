@@ -245,9 +245,9 @@ struct PairVariant {
         record(a.ev_fold_stop);
         return e;
     }
-    static cudaError_t pos_occupancy(int U, int CL, int64_t SL, int G, int* blocks) {
+    static cudaError_t pos_occupancy(int U, int CL, int64_t SL, int G, bool cluster, int* blocks) {
         (void)CL;
-        const bool cl = G > 1 && G <= kMaxPairCluster;
+        const bool cl = cluster && G > 1 && G <= kMaxPairCluster;
         const size_t sm = psmem(U, SL, G, cl);
         *blocks = 0;
         if (!HAS_POS || sm > 227 * 1024 || threads(U) > NFP) return cudaSuccess;
@@ -255,8 +255,8 @@ struct PairVariant {
         if (e != cudaSuccess) return e;
         return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, cl ? pckernel : pkernel, threads(U) + 32, sm);
     }
-    static cudaError_t occupancy(int U, int CL, int64_t SL, int G, int* blocks) {
-        const bool cl = G > 1 && G <= kMaxPairCluster;
+    static cudaError_t occupancy(int U, int CL, int64_t SL, int G, bool cluster, int* blocks) {
+        const bool cl = cluster && G > 1 && G <= kMaxPairCluster;
         const size_t sm = smem(U, CL, SL, G, cl);
         *blocks = 0;
         if (sm > 227 * 1024 || threads(U) > NT) return cudaSuccess;

@@ -9,9 +9,12 @@ namespace sigk {
 
 enum class KernelFamily : int { Path = 1, Flat = 2, Pair = 3, PFlat = 5 };  // = SIGK_FAMILY_*
 
-// Pair family: segment counts 2..kMaxPairCluster run as thread-block clusters
-// (one cluster per path, segment rows combined over distributed shared memory);
-// larger G combines through global scratch and arrival counters.
+// Pair family: in latency plans, segment counts 2..kMaxPairCluster run as
+// thread-block clusters (one cluster per path, segment rows combined over
+// distributed shared memory); otherwise (throughput plans, where clusters'
+// gang scheduling measured 7% slower back to back at C3, or G >
+// kMaxPairCluster) the rows combine through global scratch and arrival counters.
+// Both combines run the same arithmetic in the same order.
 constexpr int kMaxPairCluster = 8;
 
 // One launch of the pair family (pair_kernel.cuh): B*G CTAs of one path
@@ -56,7 +59,7 @@ struct Variant {
     cudaError_t (*occupancy)(int U, int* blocks_per_sm);
     // pair family only
     cudaError_t (*pair_launch)(const PairLaunch& a);
-    cudaError_t (*pair_occupancy)(int U, int CL, int64_t SL, int G, int* blocks_per_sm);  // 0: does not fit
+    cudaError_t (*pair_occupancy)(int U, int CL, int64_t SL, int G, bool cluster, int* blocks_per_sm);  // 0: does not fit
     int pair_units_max;  // max U/2 per CTA
     // pair family: prefix stream (B, L-1, D); G segments per path, CTA (b, g) starting from the row its
     // predecessor segment publishes in the same launch (pub/flags/epoch); cudaErrorInvalidValue when a
@@ -65,7 +68,7 @@ struct Variant {
                                  int G, void* pub, int* flags, int epoch);
     int pos_ops;          // pair family: FFMA-pipe ops per thread-step of the position-table fold (0: none)
     int pos_units_max;    // max U/2 of a position-table CTA
-    cudaError_t (*pair_pos_occupancy)(int U, int CL, int64_t SL, int G, int* blocks_per_sm);
+    cudaError_t (*pair_pos_occupancy)(int U, int CL, int64_t SL, int G, bool cluster, int* blocks_per_sm);
 };
 
 const Variant* find_variant(int d, int N, bool is_f64);  // first (smallest-Q) candidate
