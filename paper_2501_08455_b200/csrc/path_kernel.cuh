@@ -8,7 +8,8 @@
 // issued before the Horner steps of tile t, so HBM latency hides behind FFMA
 // work, and one barrier per tile suffices. When the fold ends the U chunk
 // signatures are staged into shared memory (reusing the table space) and
-// combined by the fixed-order Chen tree (merge.cuh); the path's signature is
+// combined by the per-degree prefix scan over chunks (merge.cuh: N fixed-order
+// phases of Chen-identity contributions, not a tree); the path's signature is
 // then written to HBM with coalesced stores. Nothing but X is read and nothing
 // but the final (B, D) rows is written: no intermediates touch HBM.
 #pragma once
