@@ -431,6 +431,40 @@ def run_ours(args):
     e2e_sync_s = e2e_time(0)
     e2e_s = e2e_time(sk.SIGK_ASYNC_HOST)
 
+    # c5 (strong scaling): the drop-in multi-GPU entry itself, end to end on the
+    # global batch from pinned host memory (sigk_signature_sharded_f32: one host
+    # thread and copy stream per device, rows split like rank_rows), run by rank 0
+    # over all `world` GPUs while the other ranks wait at a barrier
+    sharded = None
+    if scaling == "strong" and not args.no_sharded:
+        barrier(world)
+        if rank == 0 and torch.cuda.device_count() >= world:
+            Xg = torch.empty((B_global, L, d), dtype=torch.float32).pin_memory()
+            piece = torch.empty((min(B_global, 1024), L, d), dtype=torch.float32, device=dev)
+            for r0 in range(0, B_global, piece.shape[0]):
+                n = min(piece.shape[0], B_global - r0)
+                sk.brownian(piece[:n], seed=42, row0=r0)
+                Xg[r0:r0 + n].copy_(piece[:n])
+            del piece
+            outg = torch.empty((B_global, D), dtype=torch.float32).pin_memory()
+            st_sh = sk._Stats()
+
+            def sharded_call():
+                sk._check(lib.sigk_signature_sharded_f32(Xg.data_ptr(), B_global, L, d, N, outg.data_ptr(), world,
+                                                         C.byref(st_sh)))
+
+            sharded_call()
+            reps = 3
+            w0 = time.perf_counter()
+            for _ in range(reps):
+                sharded_call()
+            wall = time.perf_counter() - w0
+            sharded = {"value": B_global * reps / wall, "unit": "paths/s", "gpus": world, "calls": reps,
+                       "h2d_bytes_per_step": B_global * L * d * 4, "d2h_bytes_per_step": B_global * D * 4,
+                       "api": "sigk_signature_sharded_f32 (C ABI; include/sigk.h): host buffers in and out, rows "
+                              "split over the GPUs, one host thread per device; wall clock per synchronous call"}
+        barrier(world)
+
     # parity spot check of this run's output (first rows) against the oracle
     parity = None
     if rank == 0:
@@ -540,7 +574,8 @@ def run_ours(args):
                              "note": "per GPU; PCIe bounds e2e at these shapes (the kernel is ~"
                                      f"{(e2e_s / e2e_steps) / (elapsed / steps):.0f}x faster than the copies)"},
                 "synchronous": {"value": B_all * e2e_steps / e2e_sync_s, "unit": "paths/s",
-                                "api": "same call without SIGK_ASYNC_HOST (returns with each step's result)"}},
+                                "api": "same call without SIGK_ASYNC_HOST (returns with each step's result)"},
+                "sharded_entry": sharded},
         "clocks": clk.summary(),
         "gpu_launches": steps * max(1, st.launches),
     }
@@ -638,6 +673,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true", help="c5: skip the sigk_signature_sharded_f32 e2e leg")
     ap.add_argument("--chunks", type=int, default=0, help="force chunks per path (0: planned)")
     ap.add_argument("--prefix-len", type=int, default=0, help="force Q (0: planned)")
     ap.add_argument("--segments", type=int, default=0, help="pair family: force CTAs per path (0: planned)")
