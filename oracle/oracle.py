@@ -50,10 +50,12 @@ def build_port() -> str:
 
 def build_ref() -> str | None:
     """Compile the reference (only where /root/reference exists), and its acceptance
-    gate against this repository's drop-in headers and library (oracle/_ref/acceptance_dropin)."""
+    gate and doctest unit suites against this repository's drop-in headers and library
+    (oracle/_ref/acceptance_dropin, oracle/_ref/unit_tests_dropin)."""
     if os.path.isdir("/root/reference/proj/src"):
         subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
         subprocess.run(["make", "-s", "-C", HERE, "acceptance"], check=True)
+        subprocess.run(["make", "-s", "-C", HERE, "unittests"], check=True)
     return REF_SO if os.path.exists(REF_SO) else None
 
 
