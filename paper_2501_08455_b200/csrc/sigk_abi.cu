@@ -955,9 +955,20 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
                     local.segments = G;
                 }
             }
+            // chunks per path: each chunk's rows of a tile leave as one bulk copy, so
+            // the copy-out wants tiles of >= 4 rows per chunk; take the most chunks
+            // (warps) whose double-buffered stage still holds 4-step tiles (measured,
+            // C2: U 8 / TS 4 -> 73 us, 0.83 of HBM; U 10 / TS 2 82 us; U 20 / TS 1 93 us)
             int U = plan.U;
-            if (!(tun && tun->chunks > 0) && B * G <= sms)
-                U = std::max(U, (int)std::min<int64_t>(2 * plan.v->pair_units_max, std::max<int64_t>(2, SL / 8)));
+            if (!(tun && tun->chunks > 0)) {
+                if (B * G <= sms)  // idle SMs: widen the chunking (more warps on the copy-out)
+                    U = std::max(U, (int)std::min<int64_t>(2 * plan.v->pair_units_max, std::max<int64_t>(2, SL / 8)));
+                for (int u = U / 2 * 2; u >= 2; u -= 2)
+                    if (plan.v->stream_tile_steps(L, G, u) >= 4) {
+                        U = u;
+                        break;
+                    }
+            }
             for (;;) {
                 e = plan.v->stream_launch(X, B, L, U, out, s, overlap, G, pub, flags, epoch);
                 if (e != cudaErrorInvalidValue || U <= plan.U) break;

@@ -254,22 +254,23 @@ __global__ void __launch_bounds__(NT, MINB) pair_stream_kernel(const float* __re
         }
         if (bulk) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
-        // rows (chunk j, step t0+i) -> out[b, s_j + t0 + i] for real steps only; rows are
-        // dealt over the warps, one lane per warp issues (bulk groups are per thread)
-        for (int r = warp; r < U * ts; r += nwarps) {
-            const int j = r / ts, i = r - (r / ts) * ts;
+        // rows (chunk j, step t0+i) -> out[b, s_j + t0 + i] for real steps only. A
+        // chunk's rows of the tile are contiguous both in the stage and in the
+        // output, so each chunk leaves as ONE bulk copy of up to TS rows (chunks
+        // dealt over the warps, one lane per warp issues: bulk groups are per thread)
+        for (int j = warp; j < U; j += nwarps) {
             const int cs = min(j * CL, sl), ce = min(cs + CL, sl);
-            const int t = cs + t0 + i;
-            if (t >= ce) continue;
-            const float* srow = sb + ((size_t)j * TS + i) * D;
-            float* drow = ob + (int64_t)t * D;
+            const int nrows = max(0, min(ts, ce - (cs + t0)));
+            if (nrows == 0) continue;
+            const float* srow = sb + (size_t)j * TS * D;
+            float* drow = ob + (int64_t)(cs + t0) * D;
             if (bulk) {
                 if (lane == 0)
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(drow),
-                                 "r"(smem_addr(srow)), "r"((uint32_t)(D * 4))
+                                 "r"(smem_addr(srow)), "r"((uint32_t)(nrows * D * 4))
                                  : "memory");
             } else {
-                for (int c = lane; c < D; c += 32) drow[c] = srow[c];
+                for (int c = lane; c < nrows * D; c += 32) drow[c] = srow[c];
             }
         }
         if (bulk && lane == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");

@@ -268,6 +268,17 @@ struct PairVariant {
     // prefix stream: one CTA per path; the largest stage tile TS in {8, 4, 2, 1} that fits
     static constexpr auto skernel = pair_stream_kernel<DIM, DEPTH, Q, NT, MINB>;
     static std::atomic<uint64_t> ssmem_done;
+    // stage tile (steps per chunk staged before the copy-out) the stream launch uses, 0 if nothing fits
+    static int stream_tile_steps(int64_t L, int G, int U) {
+        const int64_t M = L - 1;
+        G = std::max(1, G);
+        const int64_t SL = (M + G - 1) / G;
+        U = std::max(2, U / 2 * 2);
+        const int CL = (int)((SL + U - 1) / U);
+        for (int TS = 8; TS >= 1; TS /= 2)
+            if (stream_smem_bytes<DIM, DEPTH, Q>(U, CL, raw_floats(SL), TS) <= 227 * 1024) return TS;
+        return 0;
+    }
     static cudaError_t stream_launch(const void* X, int64_t B, int64_t L, int U, void* out, cudaStream_t s,
                                      bool overlap, int G, void* pub, int* flags, int epoch) {
         const int64_t M = L - 1;
@@ -327,7 +338,7 @@ Variant make_pair_variant() {
     int chen = 0;
     for (int n = 2; n <= DEPTH; ++n) chen += (n - 2) * ipow(DIM, n);
     Variant v{DIM, DEPTH, Q, PF::P, PF::ops_per_step(), PF::loads_per_step(), chen, KernelFamily::Pair, V::NT, 0,
-              nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, 0, nullptr};
+              nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, 0, nullptr, nullptr};
     v.pair_launch = &V::launch;
     v.pair_occupancy = &V::occupancy;
     v.pair_units_max = V::NT / PF::P;
@@ -337,6 +348,7 @@ Variant make_pair_variant() {
         v.pair_pos_occupancy = &V::pos_occupancy;
     }
     v.stream_launch = &V::stream_launch;
+    v.stream_tile_steps = &V::stream_tile_steps;
     return v;
 }
 
@@ -388,7 +400,7 @@ Variant make_ipair_variant() {
     using V = IPairVariant<DIM, DEPTH, Q>;
     using F = typename V::F;
     Variant v{DIM, DEPTH, Q, F::P, F::pipe_cycles(), 0, 0, KernelFamily::PFlat, V::NT, V::T,
-              &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr};
+              &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr, nullptr};
     return v;
 }
 
@@ -401,11 +413,11 @@ Variant make_variant() {
     if constexpr (SF::P > 256) {
         using V = FlatVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Flat, V::NT, V::T,
-                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr, nullptr};
     } else {
         using V = PathVariant<Real, DIM, DEPTH, Q>;
         return Variant{DIM, DEPTH, Q, SF::P, SF::ops_per_step(), loads, chen, KernelFamily::Path, V::NTMAX, V::T,
-                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr};
+                       &V::launch, &V::occupancy, nullptr, nullptr, 0, nullptr, 0, 0, nullptr, nullptr};
     }
 }
 

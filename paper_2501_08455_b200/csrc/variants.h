@@ -69,6 +69,8 @@ struct Variant {
     int pos_ops;          // pair family: FFMA-pipe ops per thread-step of the position-table fold (0: none)
     int pos_units_max;    // max U/2 of a position-table CTA
     cudaError_t (*pair_pos_occupancy)(int U, int CL, int64_t SL, int G, bool cluster, int* blocks_per_sm);
+    // pair family: stage tile (steps) of the prefix-stream launch for (L, G, U); 0: does not fit
+    int (*stream_tile_steps)(int64_t L, int G, int U);
 };
 
 const Variant* find_variant(int d, int N, bool is_f64);  // first (smallest-Q) candidate
