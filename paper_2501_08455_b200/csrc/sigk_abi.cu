@@ -897,10 +897,6 @@ static int next_stream_epoch(int dev, cudaStream_t s) {
 }
 
 template <typename Real>
-static int parallel_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* out, bool prefix_rows,
-                           cudaStream_t s, sigk_stats* st);
-
-template <typename Real>
 static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* out, cudaStream_t s,
                          const sigk_tuning* tun, sigk_stats* st) {
     const bool is_f64 = sizeof(Real) == 8;
@@ -992,19 +988,6 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
         }
         cudaGetLastError();
     }
-    if (!done && N <= kScanMaxDepth && !(tun && (tun->force_generic || tun->family == SIGK_FAMILY_GENERIC)) &&
-        !getenv("SIGK_STREAM_GENERIC")) {
-        // no pair stream (fp64, or no pair variant): the per-degree scan formulation
-        // writes every prefix row in N parallel passes (scan_kernel.cuh), instead of
-        // one CTA per path walking the steps with a global round trip per step
-        may_overlap_previous(dev, s, X, 0, out, sizeof(Real) * B * M * D);
-        sigk_stats pst{};
-        const int rc = parallel_device<Real>(X, B, L, d, N, out, true, s, &pst);
-        if (rc != SIGK_OK) return rc;
-        local = pst;
-        local.segments = 1;
-        done = true;
-    }
     if (!done) {
         may_overlap_previous(dev, s, X, 0, out, sizeof(Real) * B * M * D);
         e = is_f64 ? launch_generic_stream_f64(X, B, L, d, N, out, s) : launch_generic_stream_f32(X, B, L, d, N, out, s);
@@ -1014,7 +997,7 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
         local.chunks = 1;
         local.fold_steps = M;
     }
-    if (local.family != SIGK_FAMILY_SCAN) local.path_steps = M;  // pass 2 / the generic walk folds every step once
+    local.path_steps = M;  // pass 2 folds every step of every path once (pair) / the generic walk does
     if (st) *st = local;
     return SIGK_OK;
 }
