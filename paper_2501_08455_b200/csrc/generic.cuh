@@ -115,15 +115,22 @@ namespace sigk {
 // t-1 (element-parallel, one barrier per step, no level ordering needed since
 // the previous state is a separate row):
 //     T_n(t)[I] = T_n(t-1)[I] + Σ_{j=1}^{n} T_{n-j}(t-1)[I / d^j] · Π_{last j digits c} δ[c] / j!
+//
+// Chunk-parallel: CTA (b, u) of a grid of B*U walks steps [u*CL, min((u+1)*CL,
+// M)) of path b, starting from `starts` row b*U + u (the signature of X[0 ..
+// u*CL], from chunk_prefix_kernel; u = 0 starts from the identity), so the
+// walk's serial length is CL instead of L-1.
 template <typename Real>
 __global__ void __launch_bounds__(256) generic_stream_kernel(const Real* __restrict__ X, int64_t L, int d, int N,
-                                                             int64_t D, Real* __restrict__ out) {
+                                                             int64_t D, Real* __restrict__ out, int U, int64_t CL,
+                                                             const Real* __restrict__ starts) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Real* dl = reinterpret_cast<Real*>(smem_raw);  // [d]
     __shared__ int64_t off[kGenericMaxDepth + 1];
     __shared__ Real invfact[kGenericMaxDepth + 1];
-    const int64_t b = blockIdx.x;
+    const int64_t b = blockIdx.x / U, u = blockIdx.x - (blockIdx.x / U) * U;
     const int64_t M = L - 1;
+    const int64_t t0 = u * CL < M ? u * CL : M, t1 = t0 + CL < M ? t0 + CL : M;
     Real* ob = out + b * M * D;
     if (threadIdx.x == 0) {
         off[0] = 0;
@@ -140,11 +147,12 @@ __global__ void __launch_bounds__(256) generic_stream_kernel(const Real* __restr
     pdl_trigger();
     pdl_wait();
     const Real* row = X + b * L * d;
-    for (int64_t t = 0; t < M; ++t) {
+    const Real* start = u > 0 ? starts + (b * U + u) * D : nullptr;
+    for (int64_t t = t0; t < t1; ++t) {
         __syncthreads();
         for (int c = threadIdx.x; c < d; c += blockDim.x) dl[c] = row[(t + 1) * d + c] - row[t * d + c];
         __syncthreads();
-        const Real* prev = t > 0 ? ob + (t - 1) * D : nullptr;
+        const Real* prev = t > t0 ? ob + (t - 1) * D : start;
         Real* cur = ob + t * D;
         for (int64_t F = threadIdx.x; F < D; F += blockDim.x) {
             int n = 1;
@@ -161,6 +169,47 @@ __global__ void __launch_bounds__(256) generic_stream_kernel(const Real* __restr
             }
             cur[F] = acc;
         }
+    }
+}
+
+// Prefixes at the chunk starts for the chunk-parallel stream: row b*U + u of
+// `starts` = C_0 ⊠ ... ⊠ C_{u-1} (u >= 1; Chen's identity,
+// tensor_algebra.cpp:80-102), from the chunk signatures C (B*U, D). One CTA
+// per path, one product per chunk, element-parallel (row 0 is not written:
+// chunk 0 starts from the identity).
+template <typename Real>
+__global__ void __launch_bounds__(256) chunk_prefix_kernel(const Real* __restrict__ C, int64_t D, int d, int N, int U,
+                                                           Real* __restrict__ starts) {
+    __shared__ int64_t off[kGenericMaxDepth + 1], pw[kGenericMaxDepth + 1];
+    if (threadIdx.x == 0) {
+        off[0] = 0;
+        pw[0] = 1;
+        for (int n = 1; n <= N; ++n) {
+            pw[n] = pw[n - 1] * d;
+            off[n] = off[n - 1] + pw[n];
+        }
+    }
+    pdl_trigger();
+    pdl_wait();
+    __syncthreads();
+    const int64_t b = blockIdx.x;
+    const Real* Cb = C + b * U * D;
+    Real* Sb = starts + b * U * D;
+    for (int u = 1; u < U; ++u) {
+        const Real* a = u > 1 ? Sb + (int64_t)(u - 1) * D : nullptr;  // P_{u-1} (identity for u = 1)
+        const Real* c = Cb + (int64_t)(u - 1) * D;                    // C_{u-1}
+        Real* o = Sb + (int64_t)u * D;
+        for (int64_t F = threadIdx.x; F < D; F += blockDim.x) {
+            int n = 1;
+            while (F >= off[n]) ++n;
+            const int64_t I = F - off[n - 1];
+            Real v = (a ? a[F] : Real(0)) + c[F];
+            if (a)
+                for (int k = 1; k < n; ++k)  // a_k ⊗ c_{n-k}
+                    v = fma(a[off[k - 1] + I / pw[n - k]], c[off[n - k - 1] + I % pw[n - k]], v);
+            o[F] = v;
+        }
+        __syncthreads();  // row u is read by the next product
     }
 }
 

@@ -989,13 +989,62 @@ static int stream_device(const Real* X, int64_t B, int64_t L, int d, int N, Real
         cudaGetLastError();
     }
     if (!done) {
+        // no pair stream (fp64, large d^N): the element-parallel walk, chunk-parallel
+        // along the sequence — chunk signatures by the fold kernels on the gathered
+        // chunks, their prefix products at every chunk start (chunk_prefix_kernel),
+        // then every (path, chunk) walks its own steps from its prefix
         may_overlap_previous(dev, s, X, 0, out, sizeof(Real) * B * M * D);
-        e = is_f64 ? launch_generic_stream_f64(X, B, L, d, N, out, s) : launch_generic_stream_f32(X, B, L, d, N, out, s);
+        const int sms = device_info(dev).sms;
+        int U = (int)std::max<int64_t>(1, std::min<int64_t>((sms * 8 + B - 1) / B, M / 32));
+        if (tun && tun->chunks > 0) U = (int)std::max<int64_t>(1, std::min<int64_t>(tun->chunks, M));
+        const int64_t CL = (M + U - 1) / U;
+        U = (int)((M + CL - 1) / CL);
+        const void* starts = nullptr;
+        std::vector<void*> tmp;
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        auto alloc = [&](int kind, size_t bytes) -> void* {
+            bool async_alloc = false;
+            void* p = segment_scratch(dev, s, kind, std::max<size_t>(bytes, 16), cap != cudaStreamCaptureStatusNone,
+                                      &async_alloc);
+            if (p && async_alloc) tmp.push_back(p);
+            return p;
+        };
+        auto release = [&] {
+            for (void* q : tmp) cudaFreeAsync(q, s);
+        };
+        int launches = 1;
+        if (U > 1) {
+            Real* Xseg = static_cast<Real*>(alloc(20, sizeof(Real) * B * U * (CL + 1) * d));
+            Real* C = static_cast<Real*>(alloc(21, sizeof(Real) * B * U * D));
+            Real* P = static_cast<Real*>(alloc(22, sizeof(Real) * B * U * D));
+            if (!Xseg || !C || !P) {
+                release();
+                return fail(SIGK_ERESOURCE, "stream chunk scratch");
+            }
+            segment_gather_kernel<Real><<<(unsigned)std::min<int64_t>(B * U, (int64_t)sms * 16), 128, 0, s>>>(
+                X, B, L, d, U, CL, Xseg);
+            sigk_stats cst{};
+            sigk_tuning ct{};
+            ct.no_overlap = 1;
+            const int rc = run_device<Real>(Xseg, B * U, CL + 1, d, N, C, s, &ct, &cst);
+            if (rc != SIGK_OK) {
+                release();
+                return rc;
+            }
+            chunk_prefix_kernel<Real><<<(unsigned)B, 256, 0, s>>>(C, D, d, N, U, P);
+            starts = P;
+            launches += 2 + cst.launches;
+        }
+        e = is_f64 ? launch_generic_stream_f64(X, B, L, d, N, out, s, U, CL, starts)
+                   : launch_generic_stream_f32(X, B, L, d, N, out, s, U, CL, starts);
+        release();
         if (e != cudaSuccess) return cuda_fail(e, "generic stream launch");
         local.family = SIGK_FAMILY_GENERIC;
         local.prefix_len = -1;
-        local.chunks = 1;
-        local.fold_steps = M;
+        local.chunks = U;
+        local.fold_steps = CL;
+        local.launches = launches;
     }
     local.path_steps = M;  // pass 2 folds every step of every path once (pair) / the generic walk does
     if (st) *st = local;
@@ -1699,22 +1748,25 @@ cudaError_t launch_generic_f64(const void* X, int64_t B, int64_t L, int d, int N
     return gen<double>(X, B, L, d, N, out, s);
 }
 template <typename Real>
-static cudaError_t gen_stream(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s) {
+static cudaError_t gen_stream(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s, int U,
+                              int64_t CL, const void* starts) {
     const int64_t D = level_off(d, N);
     if (N > kGenericMaxDepth) return cudaErrorInvalidValue;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)B);
+    cfg.gridDim = dim3((unsigned)(B * U));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = sizeof(Real) * d;
     cfg.stream = s;
     return cudaLaunchKernelEx(&cfg, generic_stream_kernel<Real>, static_cast<const Real*>(X), L, d, N, D,
-                              static_cast<Real*>(out));
+                              static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts));
 }
-cudaError_t launch_generic_stream_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s) {
-    return gen_stream<float>(X, B, L, d, N, out, s);
+cudaError_t launch_generic_stream_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s,
+                                      int U, int64_t CL, const void* starts) {
+    return gen_stream<float>(X, B, L, d, N, out, s, U, CL, starts);
 }
-cudaError_t launch_generic_stream_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s) {
-    return gen_stream<double>(X, B, L, d, N, out, s);
+cudaError_t launch_generic_stream_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s,
+                                      int U, int64_t CL, const void* starts) {
+    return gen_stream<double>(X, B, L, d, N, out, s, U, CL, starts);
 }
 cudaError_t launch_brownian_f32(void* X, int64_t B, int64_t L, int d, uint64_t seed, int64_t row0, cudaStream_t s) {
     return brown<float>(X, B, L, d, seed, row0, s);

@@ -77,8 +77,12 @@ const Variant* find_variant(int d, int N, bool is_f64);  // first (smallest-Q) c
 int find_variants(int d, int N, bool is_f64, const Variant** out, int max);
 cudaError_t launch_generic_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
 cudaError_t launch_generic_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
-cudaError_t launch_generic_stream_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
-cudaError_t launch_generic_stream_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s);
+// chunk-parallel generic stream: U chunks of CL steps per path, chunk u > 0 starting from
+// row b*U + u of `starts` (null when U == 1)
+cudaError_t launch_generic_stream_f32(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s,
+                                      int U, int64_t CL, const void* starts);
+cudaError_t launch_generic_stream_f64(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s,
+                                      int U, int64_t CL, const void* starts);
 cudaError_t launch_brownian_f32(void* X, int64_t B, int64_t L, int d, uint64_t seed, int64_t row0, cudaStream_t s);
 cudaError_t launch_brownian_f64(void* X, int64_t B, int64_t L, int d, uint64_t seed, int64_t row0, cudaStream_t s);
 
