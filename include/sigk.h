@@ -137,12 +137,17 @@ typedef struct sigk_tuning {
     int32_t mode;           /* SIGK_MODE_*: what the fold plan optimises (0: automatic) */
     int32_t fold_variant;   /* pair family: 0 planned, 1 register-table fold, 2 position-table
                                fold with a producer warp (sigk_stats.family stays PAIR) */
+    int32_t cluster;        /* pair family, 2 <= segments <= 8: 1 = the segment CTAs of a path form a
+                               thread-block cluster and combine over distributed shared memory
+                               (no scratch, no arrival counters); 0 = global-scratch combine.
+                               Same arithmetic, same results; measured slower on B200 in both
+                               regimes, so opt-in. */
 } sigk_tuning;
 
 /* sigk_tuning.mode. THROUGHPUT plans for back-to-back calls on a stream (launches
  * overlap through programmatic dependent launch: per-CTA fixed phases hide behind
  * other CTAs' folds); LATENCY plans for a call that runs alone (all CTAs start
- * together: more warps per SM, wide CTAs, thread-block-cluster segment combine).
+ * together: more chunks per path, so more warps per SM).
  * AUTO = THROUGHPUT for device-buffer calls, LATENCY for synchronous host-buffer
  * calls. The plan (hence the rounding of the result) is a deterministic function
  * of the call's arguments and mode. */

@@ -62,7 +62,8 @@ class _Tuning(C.Structure):
     _fields_ = [("chunks", C.c_int32), ("force_generic", C.c_int32), ("plan_rows", C.c_int64),
                 ("fold_event_start", C.c_void_p), ("fold_event_stop", C.c_void_p), ("prefix_len", C.c_int32),
                 ("no_overlap", C.c_int32), ("segments", C.c_int32), ("family", C.c_int32),
-                ("phase_buf", C.c_void_p), ("mode", C.c_int32), ("fold_variant", C.c_int32)]
+                ("phase_buf", C.c_void_p), ("mode", C.c_int32), ("fold_variant", C.c_int32),
+                ("cluster", C.c_int32)]
 
 
 MODE_AUTO, MODE_THROUGHPUT, MODE_LATENCY = 0, 1, 2  # sigk_tuning.mode (include/sigk.h SIGK_MODE_*)
@@ -284,10 +285,10 @@ def _check_out(out, shape, like, *, pinned: bool = False):
 
 def _run(paths, depth: int, stats: KernelStats | None, chunks: int = 0, force_generic: bool = False,
          out=None, plan_rows: int = 0, prefix_len: int = 0, segments: int = 0, family: int = 0, mode: int = 0,
-         fold_variant: int = 0):
+         fold_variant: int = 0, cluster: int = 0):
     st = _Stats()
     tun = _Tuning(chunks=chunks, force_generic=int(force_generic), plan_rows=plan_rows, prefix_len=prefix_len,
-                  segments=segments, family=family, mode=mode, fold_variant=fold_variant)
+                  segments=segments, family=family, mode=mode, fold_variant=fold_variant, cluster=cluster)
     if _is_torch(paths):
         import torch
 
@@ -368,7 +369,7 @@ def _seq_len(paths) -> int:
 def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,
               stats: KernelStats | None = None, *, chunks: int = 0, out=None, plan_rows: int = 0,
               prefix_len: int = 0, segments: int = 0, family: int = 0, mode: int = MODE_AUTO,
-              fold_variant: int = 0):
+              fold_variant: int = 0, cluster: int = 0):
     """Reference ``sigkit::signature`` (kernels.cpp:200-206): (B, L, d) -> (B, D).
 
     ``kernel``/``caps`` dispatch like the reference (select_kernel,
@@ -381,12 +382,13 @@ def signature(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: Exe
     ``mode`` picks what the plan optimises (MODE_THROUGHPUT: back-to-back calls,
     MODE_LATENCY: a call that runs alone; MODE_AUTO: latency for numpy inputs,
     throughput for device tensors); ``fold_variant`` pins the pair family's fold
-    (1 register table, 2 position table with a producer warp; 0 planned).
+    (1 register table, 2 position table with a producer warp; 0 planned); ``cluster=1``
+    combines 2..8 segments of a path inside a thread-block cluster (opt-in).
     """
     if select_kernel(kernel, caps or ExecutionCaps.detect(), _seq_len(paths)) == KernelKind.Parallel:
         return signature_parallel(paths, depth, stats, out=out)
     return _run(paths, depth, stats, chunks=chunks, out=out, plan_rows=plan_rows, prefix_len=prefix_len,
-                segments=segments, family=family, mode=mode, fold_variant=fold_variant)
+                segments=segments, family=family, mode=mode, fold_variant=fold_variant, cluster=cluster)
 
 
 def signature_stream(paths, depth: int, kernel: KernelKind = KernelKind.Auto, caps: ExecutionCaps | None = None,

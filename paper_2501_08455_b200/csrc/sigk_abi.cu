@@ -207,6 +207,7 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
     const int fU = tun ? tun->chunks : 0;
     const int fG = tun ? tun->segments : 0;
     const bool latency = tun && tun->mode == SIGK_MODE_LATENCY;
+    const bool use_cluster = tun && tun->cluster;
     const int fvar = tun ? tun->fold_variant : 0;
     bool have_pair = false;
     for (int k = 0; k < nc; ++k)
@@ -262,8 +263,8 @@ static Plan plan_launch(int d, int N, bool is_f64, int64_t B, int64_t M, int sms
                         if (pos && (v.pos_ops == 0 || U / 2 > v.pos_units_max || fvar != 2)) continue;
                         if (!pos && fvar == 2) continue;
                         int occ = 0;
-                        if ((pos ? v.pair_pos_occupancy(U, CL, SL, G, latency, &occ)
-                                 : v.pair_occupancy(U, CL, SL, G, latency, &occ)) !=
+                        if ((pos ? v.pair_pos_occupancy(U, CL, SL, G, use_cluster, &occ)
+                                 : v.pair_occupancy(U, CL, SL, G, use_cluster, &occ)) !=
                                 cudaSuccess ||
                             occ < 1)
                             continue;
@@ -492,7 +493,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         void* rows = nullptr;
         void* counters = nullptr;
         bool async_rows = false, async_ctr = false;
-        const bool cluster = G > 1 && G <= kMaxPairCluster && tun && tun->mode == SIGK_MODE_LATENCY;
+        const bool cluster = G > 1 && G <= kMaxPairCluster && tun && tun->cluster;
         if (G > 1 && !cluster) {
             if (cap == cudaStreamCaptureStatusNone) cudaStreamIsCapturing(s, &cap);
             const bool capt = cap == cudaStreamCaptureStatusActive;

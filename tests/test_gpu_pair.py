@@ -197,3 +197,16 @@ def test_position_table_fold_headline_and_batch_invariance(sk):
     assert max(level_errors(got, ref, 5, 4)) <= F32_TOL
     one, _ = pair(sk, X[5:6], 4, fold_variant=2, chunks=10, segments=1)
     assert np.array_equal(one[0], got[5])
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_cluster_segment_combine(sk, G):
+    # opt-in thread-block-cluster (DSMEM) segment combine: same arithmetic and
+    # order as the global-scratch combine, hence bitwise the same rows
+    X = brownian(10, 1201, 5, seed=300 + G)
+    ref = oracle32(X, 4)
+    got, st = pair(sk, X, 4, segments=G, cluster=1)
+    assert st.segments == G
+    assert max(level_errors(got, ref, 5, 4)) <= F32_TOL
+    glob, _ = pair(sk, X, 4, segments=G, chunks=st.chunks)
+    assert np.array_equal(got, glob)
