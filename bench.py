@@ -309,6 +309,8 @@ def run_ours(args):
     # FFMA-pipe peak on this GPU (roofline denominator)
     import ctypes as C
 
+    lib_span = sk.lib()
+
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     sink = torch.empty(sms * 8 * 256, dtype=torch.float32, device=dev)
     fl = C.c_double(0)
@@ -388,6 +390,29 @@ def run_ours(args):
     stream.synchronize()
     lat_ms = [a.elapsed_time(b) for a, b in ev_lat]
     lat_s = max_over_ranks(sum(lat_ms) / len(lat_ms) * 1e-3, world)
+
+    # device-side span of one launch alone (pair family): %globaltimer stamps at every
+    # CTA's entry and exit (sigk_tuning.phase_buf), first entry to last exit — the
+    # kernel's execution without the launch latency the event bracket includes
+    span_ms = {}
+    if st.family == sk.FAMILY_PAIR:
+        for mode_name, mode in (("throughput_plan", 0), ("latency_plan", sk.MODE_LATENCY)):
+            p = sk.plan(B, L, d, N, mode=mode, **{k: v for k, v in TUNE.items() if k != "mode"})
+            ph = torch.zeros((B * p.segments, 12), dtype=torch.int64, device=dev)
+            spans = []
+            for _ in range(5):
+                with torch.cuda.stream(stream):
+                    flush.fill_(4.0)
+                    tun = sk._Tuning(**TUNE)
+                    tun.mode = mode
+                    tun.phase_buf = C.c_void_p(ph.data_ptr())
+                    sk._check(lib_span.sigk_signature_f32(pool[0].data_ptr(), B, L, d, N, out.data_ptr(),
+                                                          sk.SIGK_X_ON_DEVICE | sk.SIGK_OUT_ON_DEVICE,
+                                                          C.c_void_p(stream.cuda_stream), C.byref(tun), None))
+                stream.synchronize()
+                w = ph[:, 10:12].cpu()
+                spans.append(float((w[:, 1].max() - w[:, 0].min()).item()) * 1e-6)
+            span_ms[mode_name] = max_over_ranks(sorted(spans)[len(spans) // 2], world)
 
     # single-launch (non-graph) latency of one step, for reference
     with torch.cuda.stream(stream):
@@ -554,6 +579,11 @@ def run_ours(args):
                                     "graph replay after an L2 flush (no launch overlap); includes the launch "
                                     "latency of an idle GPU (a ~1 us C1 fold measures ~8 us this way, "
                                     "profiles/r02/mode_probe.txt)",
+                            "device_span_ms": span_ms,
+                            "device_span_frac": {k: B * flops_path / (v * 1e-3) / 1e12 / peak for k, v in span_ms.items()}
+                            if peak else None,
+                            "device_span_from": "one launch alone after an L2 flush: %globaltimer at every CTA's "
+                                                "entry and exit, first entry to last exit (median of 5)",
                             "latency_plan": {"kernel_ms": lat_s * 1e3,
                                              "frac": B * flops_path / lat_s / 1e12 / peak if peak else None,
                                              "chunks": lat_plan.chunks, "segments": lat_plan.segments,
