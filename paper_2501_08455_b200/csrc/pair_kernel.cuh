@@ -388,8 +388,43 @@ __device__ __forceinline__ void fused_scan(const CombineSmem<d, N, P1S>& S, int 
                 P[a] = (a == 1) ? S.p10[idx[1]] : (S.p0 ? __ldcg(S.p0 + level_off(d, a - 1) + idx[a]) : 0.f);  // p0: a previous launch's output, via L2
                 if (wr[a]) S.pf[level_off(d, a - 1) + idx[a]] = P[a];
             }
+            // long scans (U >= 16, the latency plans): blocks of V pieces whose inputs
+            // (Y entries, chain factors: independent of P) are all loaded before the
+            // block's pf stores, so only the FMA recurrence through P is serial;
+            // short scans keep the plain walk (measured: the blocked form costs the
+            // back-to-back U = 10 plan 1%, saves ~1 K cycles at U = 20)
+            constexpr int V = 4;
+            const int jb = U >= 16 ? U - U % V : 0;
+            for (int j0 = 0; j0 < jb; j0 += V) {
+                float yv[V][E + 1], cv[V][E + 1][E + 1];
+#pragma unroll
+                for (int u = 0; u < V; ++u) {
+#pragma unroll
+                    for (int a = A0; a <= E; ++a) {
+                        yv[u][a] = S.y(j0 + u, a, idx[a]);
+#pragma unroll
+                        for (int b = A0; b < a; ++b) cv[u][a][b] = c_chain<d, N, P1S>(S, j0 + u, dg, a, b);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < V; ++u) {
+                    float nP[E + 1];
+#pragma unroll
+                    for (int a = A0; a <= E; ++a) {
+                        float x = P[a] + yv[u][a];
+#pragma unroll
+                        for (int b = A0; b < a; ++b) x = fmaf(P[b], cv[u][a][b], x);
+                        nP[a] = x;
+                    }
+#pragma unroll
+                    for (int a = A0; a <= E; ++a) {
+                        P[a] = nP[a];
+                        if (wr[a]) S.pf[(size_t)(j0 + u + 1) * DL + level_off(d, a - 1) + idx[a]] = P[a];
+                    }
+                }
+            }
 #pragma unroll 4
-            for (int j = 0; j < U; ++j) {
+            for (int j = jb; j < U; ++j) {
                 float nP[E + 1];
 #pragma unroll
                 for (int a = A0; a <= E; ++a) {
