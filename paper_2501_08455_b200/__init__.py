@@ -465,6 +465,44 @@ def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.
     return grad
 
 
+class _SignatureFn:
+    """torch.autograd.Function over the GPU forward and reverse mode (built lazily so
+    importing the package does not import torch)."""
+    _cls = None
+
+    @classmethod
+    def get(cls):
+        if cls._cls is None:
+            import torch
+
+            class SignatureFunction(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, X, depth):
+                    ctx.depth = depth
+                    ctx.save_for_backward(X)
+                    return _run(X, depth, None)
+
+                @staticmethod
+                def backward(ctx, grad_out):
+                    (X,) = ctx.saved_tensors
+                    return signature_vjp(X, ctx.depth, grad_out.contiguous()), None
+
+            cls._cls = SignatureFunction
+        return cls._cls
+
+
+def signature_autograd(paths, depth: int):
+    """Differentiable signature for CUDA torch tensors (B, L, d) -> (B, D): the forward
+    is ``signature`` (chunked GPU fold), the backward ``signature_vjp`` (GPU reverse
+    mode) — the signature layer of the paper's training setup (§3.2) as a
+    ``torch.autograd.Function``; float32 or float64."""
+    if not _is_torch(paths) or not paths.is_cuda:
+        raise DomainError("signature_autograd needs a CUDA torch tensor")
+    _validate_shape(paths.shape, depth)
+    _torch_dtype_ok(paths)
+    return _SignatureFn.get().apply(paths.contiguous(), depth)
+
+
 def signature_sequential(paths, depth: int, stats: KernelStats | None = None, **kw):
     """Reference ``signature_sequential`` (kernels.cpp:106-122): the chunked Chen fold."""
     return _run(paths, depth, stats, **kw)
@@ -589,7 +627,7 @@ __all__ = [
     "DomainError", "ResourceError", "TrainingError", "DeviceError", "KernelKind", "KernelStats", "ExecutionCaps", "kernel_name",
     "kernel_from_name", "select_kernel", "sig_dim", "level_offsets", "level_sizes", "signature",
     "signature_sequential", "signature_parallel", "signature_generic", "signature_sharded", "brownian",
-    "signature_stream", "signature_vjp", "TrainConfig", "train", "increments", "scaled_increments", "signature_bruteforce",
+    "signature_stream", "signature_vjp", "signature_autograd", "TrainConfig", "train", "increments", "scaled_increments", "signature_bruteforce",
     "has_fast_variant", "lib", "plan", "FAMILY_AUTO", "FAMILY_PATH", "FAMILY_FLAT", "FAMILY_PAIR",
     "FAMILY_GENERIC", "FAMILY_PFLAT", "FAMILY_SCAN", "FAMILY_NAMES", "MODE_AUTO", "MODE_THROUGHPUT", "MODE_LATENCY", "SIGK_X_ON_DEVICE", "SIGK_OUT_ON_DEVICE",
     "SIGK_ASYNC_HOST", "SIGK_PREFIX_ROWS", "DEFAULT_PARALLEL_MEMORY_CAP",
