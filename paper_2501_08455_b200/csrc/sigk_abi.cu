@@ -634,6 +634,7 @@ struct AsyncRing {
     void* p[R] = {};
     size_t n[R] = {};
     cudaStream_t hs = nullptr, cs = nullptr, ds = nullptr;  // H2D, kernels, D2H
+    cudaStream_t hs2 = nullptr;  // second H2D stream: consecutive calls' inputs on both copy engines
     cudaEvent_t h2d[R] = {}, kdone[R] = {}, d2h[R] = {};
     bool used[R] = {};
     unsigned next = 0;
@@ -701,6 +702,7 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
         std::lock_guard<std::mutex> lock(rg.mu);
         if (!rg.hs) {
             cudaStreamCreateWithFlags(&rg.hs, cudaStreamNonBlocking);
+            cudaStreamCreateWithFlags(&rg.hs2, cudaStreamNonBlocking);
             cudaStreamCreateWithFlags(&rg.cs, cudaStreamNonBlocking);
             cudaStreamCreateWithFlags(&rg.ds, cudaStreamNonBlocking);
             for (int k = 0; k < AsyncRing::R; ++k) {
@@ -729,10 +731,13 @@ static int signature_impl(const Real* X, size_t B, size_t L, int d, int N, Real*
         // H2D on the copy stream, ordered only after the slot's last reader: X is
         // host data that is complete at call time, so it need not wait for the
         // caller's queued work (that would serialise consecutive calls)
-        if (rg.used[k]) cudaStreamWaitEvent(rg.hs, rg.kdone[k], 0);
-        e = cudaMemcpyAsync(xbuf, X, xbytes, cudaMemcpyHostToDevice, rg.hs);
+        // alternate calls between two H2D streams (measured on B200: 48.9 -> 51.2 GB/s
+        // aggregate for 2.56 MB copies, tools/h2d_probe.py)
+        cudaStream_t hs = (rg.next & 1) ? rg.hs2 : rg.hs;
+        if (rg.used[k]) cudaStreamWaitEvent(hs, rg.kdone[k], 0);
+        e = cudaMemcpyAsync(xbuf, X, xbytes, cudaMemcpyHostToDevice, hs);
         if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
-        cudaEventRecord(rg.h2d[k], rg.hs);
+        cudaEventRecord(rg.h2d[k], hs);
         cudaStreamWaitEvent(rg.cs, rg.h2d[k], 0);
         if (rg.used[k]) cudaStreamWaitEvent(rg.cs, rg.d2h[k], 0);  // obuf drained
         rc = run_device<Real>(xbuf, (int64_t)B, (int64_t)L, d, N, obuf, rg.cs, tun, st);
