@@ -420,10 +420,9 @@ static void* segment_scratch(int dev, cudaStream_t s, int kind, size_t bytes, bo
 static int64_t covered_steps(int64_t M, int64_t G, int64_t U) {
     const int64_t SL = (M + G - 1) / G, CL = (SL + U - 1) / U;
     int64_t n = 0;
-    for (int64_t g = 0; g < G; ++g) {
+    for (int64_t g = 0; g < G; ++g) {  // U chunks of CL steps cover min(segment, U*CL) of each segment
         const int64_t s0 = std::min(M, g * SL), s1 = std::min(M, s0 + SL);
-        for (int64_t u = 0; u < U; ++u)
-            n += std::max<int64_t>(0, std::min(s1, s0 + (u + 1) * CL) - std::min(s1, s0 + u * CL));
+        n += std::min(s1 - s0, U * CL);
     }
     return n;
 }
