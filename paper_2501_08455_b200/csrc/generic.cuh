@@ -172,6 +172,93 @@ __global__ void __launch_bounds__(256) generic_stream_kernel(const Real* __restr
     }
 }
 
+// The same walk for small signatures (D <= 1024, d <= 16): one thread per
+// entry (block = D rounded up to a warp), its index data in registers — the
+// degree, the trailing digits (4 bits each) and the offsets of the NM
+// lower-degree entries it multiplies — so a step costs loads and FMAs only,
+// no integer division; the running row is double-buffered in shared memory
+// and the chunk's points are staged once, so a step touches global memory
+// only to store its row.
+template <typename Real, int NM>
+__global__ void __launch_bounds__(1024) generic_stream_small_kernel(const Real* __restrict__ X, int64_t L, int d, int N,
+                                                                    int64_t D, Real* __restrict__ out, int U, int64_t CL,
+                                                                    const Real* __restrict__ starts) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* dl = reinterpret_cast<Real*>(smem_raw);  // [d]
+    __shared__ Real invfact[NM + 1];
+    const int64_t b = blockIdx.x / U, u = blockIdx.x - (blockIdx.x / U) * U;
+    const int64_t M = L - 1;
+    const int64_t t0 = u * CL < M ? u * CL : M, t1 = t0 + CL < M ? t0 + CL : M;
+    Real* ob = out + b * M * D;
+    if (threadIdx.x == 0) {
+        Real f = 1;
+        invfact[0] = 1;
+        for (int n = 1; n <= N; ++n) {
+            f *= Real(n);
+            invfact[n] = Real(1) / f;
+        }
+    }
+    const int F = (int)threadIdx.x;
+    int deg = 0;
+    uint32_t digs = 0;
+    int lo[NM];
+#pragma unroll
+    for (int j = 0; j < NM; ++j) lo[j] = 0;
+    if (F < D) {
+        int n = 1, off0 = 0, sz = d;  // level n occupies [off0, off0 + sz)
+        while (F >= off0 + sz) {
+            off0 += sz;
+            sz *= d;
+            ++n;
+        }
+        deg = n;
+        int rem = F - off0;
+#pragma unroll
+        for (int j = 1; j <= NM; ++j) {
+            if (j <= n) {
+                digs |= (uint32_t)(rem % d) << (4 * (j - 1));
+                rem /= d;
+                int offl = 0, p = 1;  // entry I / d^j of level n - j starts at off(n - j - 1)
+                for (int m = 1; m < n - j; ++m) {
+                    p *= d;
+                    offl += p;
+                }
+                lo[j - 1] = offl + rem;
+            }
+        }
+    }
+    pdl_trigger();
+    pdl_wait();
+    const Real* row = X + b * L * d;
+    Real* rows = dl + 16;      // [2][D]
+    Real* pts = rows + 2 * D;  // X[t0 .. t1]
+    const Real* start = u > 0 ? starts + (b * U + u) * D : nullptr;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) rows[i] = start ? start[i] : Real(0);
+    for (int64_t i = threadIdx.x; i < (t1 - t0 + 1) * d; i += blockDim.x) pts[i] = row[t0 * d + i];
+    for (int64_t t = t0; t < t1; ++t) {
+        __syncthreads();
+        const Real* pt = pts + (t - t0) * d;
+        for (int c = threadIdx.x; c < d; c += blockDim.x) dl[c] = pt[d + c] - pt[c];
+        __syncthreads();
+        const int par = (int)((t - t0) & 1);
+        const Real* prev = rows + par * D;
+        if (deg > 0) {
+            Real acc = prev[F];
+            Real e = 1;
+#pragma unroll
+            for (int j = 1; j <= NM; ++j) {
+                if (j <= deg) {
+                    e *= dl[(digs >> (4 * (j - 1))) & 15u];
+                    const Real lower = (j < deg) ? prev[lo[j - 1]] : Real(1);
+                    acc = fma(lower, e * invfact[j], acc);
+                }
+            }
+            rows[(1 - par) * D + F] = acc;
+            ob[t * D + F] = acc;
+        }
+    }
+}
+
 // Prefixes at the chunk starts for the chunk-parallel stream: row b*U + u of
 // `starts` = C_0 ⊠ ... ⊠ C_{u-1} (u >= 1; Chen's identity,
 // tensor_algebra.cpp:80-102), from the chunk signatures C (B*U, D). One CTA

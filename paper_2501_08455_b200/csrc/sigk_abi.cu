@@ -1762,6 +1762,16 @@ static cudaError_t gen_stream(const void* X, int64_t B, int64_t L, int d, int N,
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = sizeof(Real) * d;
     cfg.stream = s;
+    const size_t small_smem = sizeof(Real) * (16 + 2 * D + (CL + 1) * (int64_t)d);
+    if (D <= 1024 && N <= 8 && d <= 16 && small_smem <= 48 * 1024) {  // one thread per entry, rows + points in smem
+        cfg.blockDim = dim3((unsigned)((D + 31) / 32 * 32));
+        cfg.dynamicSmemBytes = small_smem;
+        if (N <= 4)
+            return cudaLaunchKernelEx(&cfg, generic_stream_small_kernel<Real, 4>, static_cast<const Real*>(X), L, d, N,
+                                      D, static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts));
+        return cudaLaunchKernelEx(&cfg, generic_stream_small_kernel<Real, 8>, static_cast<const Real*>(X), L, d, N, D,
+                                  static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts));
+    }
     return cudaLaunchKernelEx(&cfg, generic_stream_kernel<Real>, static_cast<const Real*>(X), L, d, N, D,
                               static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts));
 }
