@@ -179,10 +179,14 @@ __global__ void __launch_bounds__(256) generic_stream_kernel(const Real* __restr
 // no integer division; the running row is double-buffered in shared memory
 // and the chunk's points are staged once, so a step touches global memory
 // only to store its row.
+// final_rows != null: signature mode — no row per step; the chunk's own
+// signature (walked from the identity when starts == null) goes to row
+// b*U + u of final_rows.
 template <typename Real, int NM>
 __global__ void __launch_bounds__(1024) generic_stream_small_kernel(const Real* __restrict__ X, int64_t L, int d, int N,
                                                                     int64_t D, Real* __restrict__ out, int U, int64_t CL,
-                                                                    const Real* __restrict__ starts) {
+                                                                    const Real* __restrict__ starts,
+                                                                    Real* __restrict__ final_rows) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Real* dl = reinterpret_cast<Real*>(smem_raw);  // [d]
     __shared__ Real invfact[NM + 1];
@@ -254,8 +258,76 @@ __global__ void __launch_bounds__(1024) generic_stream_small_kernel(const Real* 
                 }
             }
             rows[(1 - par) * D + F] = acc;
-            ob[t * D + F] = acc;
+            if (!final_rows) ob[t * D + F] = acc;
         }
+    }
+    if (final_rows && F < D) final_rows[(b * U + u) * D + F] = rows[((t1 - t0) & 1) * D + F];
+}
+
+// The chunk walk for larger signatures or depths (any D whose two rows and the
+// chunk's points fit shared memory, N <= 16): 1024 threads, entries strided
+// over them, index data recomputed per step in 32-bit arithmetic; rows and
+// points in shared memory as above. final_rows as generic_stream_small_kernel.
+template <typename Real>
+__global__ void __launch_bounds__(1024) generic_walk_kernel(const Real* __restrict__ X, int64_t L, int d, int N, int64_t D,
+                                                            Real* __restrict__ out, int U, int64_t CL,
+                                                            const Real* __restrict__ starts,
+                                                            Real* __restrict__ final_rows) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* dl = reinterpret_cast<Real*>(smem_raw);  // [d] (<= 16)
+    __shared__ int off[kGenericMaxDepth + 1];
+    __shared__ Real invfact[kGenericMaxDepth + 1];
+    const int64_t b = blockIdx.x / U, u = blockIdx.x - (blockIdx.x / U) * U;
+    const int64_t M = L - 1;
+    const int64_t t0 = u * CL < M ? u * CL : M, t1 = t0 + CL < M ? t0 + CL : M;
+    Real* ob = out ? out + b * M * D : nullptr;
+    if (threadIdx.x == 0) {
+        off[0] = 0;
+        int p = 1;
+        Real f = 1;
+        invfact[0] = 1;
+        for (int n = 1; n <= N; ++n) {
+            p *= d;
+            off[n] = off[n - 1] + p;
+            f *= Real(n);
+            invfact[n] = Real(1) / f;
+        }
+    }
+    pdl_trigger();
+    pdl_wait();
+    const Real* row = X + b * L * d;
+    Real* rows = dl + 16;      // [2][D]
+    Real* pts = rows + 2 * D;  // X[t0 .. t1]
+    const Real* start = u > 0 && starts ? starts + (b * U + u) * D : nullptr;
+    for (int64_t i = threadIdx.x; i < D; i += blockDim.x) rows[i] = start ? start[i] : Real(0);
+    for (int64_t i = threadIdx.x; i < (t1 - t0 + 1) * d; i += blockDim.x) pts[i] = row[t0 * d + i];
+    for (int64_t t = t0; t < t1; ++t) {
+        __syncthreads();
+        const Real* pt = pts + (t - t0) * d;
+        for (int c = threadIdx.x; c < d; c += blockDim.x) dl[c] = pt[d + c] - pt[c];
+        __syncthreads();
+        const int par = (int)((t - t0) & 1);
+        const Real* prev = rows + par * D;
+        Real* nxt = rows + (1 - par) * D;
+        for (int F = threadIdx.x; F < (int)D; F += blockDim.x) {
+            int n = 1;
+            while (F >= off[n]) ++n;
+            int rem = F - off[n - 1];
+            Real acc = prev[F], e = 1;
+            for (int j = 1; j <= n; ++j) {
+                e *= dl[rem % d];
+                rem /= d;
+                const Real lower = (j < n) ? prev[off[n - j - 1] + rem] : Real(1);
+                acc = fma(lower, e * invfact[j], acc);
+            }
+            nxt[F] = acc;
+            if (!final_rows) ob[t * D + F] = acc;
+        }
+    }
+    if (final_rows) {
+        __syncthreads();
+        const Real* fin = rows + ((t1 - t0) & 1) * D;
+        for (int64_t F = threadIdx.x; F < D; F += blockDim.x) final_rows[(b * U + u) * D + F] = fin[F];
     }
 }
 
@@ -298,6 +370,48 @@ __global__ void __launch_bounds__(256) chunk_prefix_kernel(const Real* __restric
         }
         __syncthreads();  // row u is read by the next product
     }
+}
+
+// Signature of each path from its U chunk signatures (rows b*U .. b*U+U-1 of
+// C): out[b] = C_0 ⊠ C_1 ⊠ ... ⊠ C_{U-1}, left to right in a fixed order
+// (Chen's identity, tensor_algebra.cpp:80-102). One CTA per path, the running
+// product double-buffered in shared memory (2 D values).
+template <typename Real>
+__global__ void __launch_bounds__(256) chunk_product_kernel(const Real* __restrict__ C, int64_t D, int d, int N, int U,
+                                                            Real* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* acc = reinterpret_cast<Real*>(smem_raw);  // [2][D]
+    __shared__ int64_t off[kGenericMaxDepth + 1], pw[kGenericMaxDepth + 1];
+    if (threadIdx.x == 0) {
+        off[0] = 0;
+        pw[0] = 1;
+        for (int n = 1; n <= N; ++n) {
+            pw[n] = pw[n - 1] * d;
+            off[n] = off[n - 1] + pw[n];
+        }
+    }
+    pdl_trigger();
+    pdl_wait();
+    const int64_t b = blockIdx.x;
+    const Real* Cb = C + b * U * D;
+    for (int64_t F = threadIdx.x; F < D; F += blockDim.x) acc[F] = Cb[F];
+    __syncthreads();
+    for (int u = 1; u < U; ++u) {
+        const Real* a = acc + ((u - 1) & 1) * D;
+        Real* o = acc + (u & 1) * D;
+        const Real* c = Cb + (int64_t)u * D;
+        for (int64_t F = threadIdx.x; F < D; F += blockDim.x) {
+            int n = 1;
+            while (F >= off[n]) ++n;
+            const int64_t I = F - off[n - 1];
+            Real v = a[F] + c[F];
+            for (int k = 1; k < n; ++k) v = fma(a[off[k - 1] + I / pw[n - k]], c[off[n - k - 1] + I % pw[n - k]], v);
+            o[F] = v;
+        }
+        __syncthreads();
+    }
+    const Real* fin = acc + ((U - 1) & 1) * D;
+    for (int64_t F = threadIdx.x; F < D; F += blockDim.x) out[b * D + F] = fin[F];
 }
 
 }  // namespace sigk

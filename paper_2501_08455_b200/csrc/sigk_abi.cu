@@ -1736,6 +1736,59 @@ template <typename Real>
 static cudaError_t gen(const void* X, int64_t B, int64_t L, int d, int N, void* out, cudaStream_t s) {
     const int64_t D = level_off(d, N);
     if (N > kGenericMaxDepth) return cudaErrorInvalidValue;
+    const int64_t M = L - 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int sms = device_info(dev).sms;
+    // small signatures: chunk-parallel one-thread-per-entry walks (each (path, chunk)
+    // folds its own steps from the identity, generic_stream_small_kernel in signature
+    // mode), then the fixed-order product of the chunk signatures per path
+    const bool small = D <= 1024 && N <= 8 && d <= 16;
+    if (d <= 16 && M >= 1) {
+        int U = (int)std::max<int64_t>(1, std::min<int64_t>((sms * 8 + B - 1) / B, M / 32));
+        const int64_t CL = (M + U - 1) / U;
+        U = (int)((M + CL - 1) / CL);
+        const size_t smem = sizeof(Real) * (16 + 2 * D + (CL + 1) * (int64_t)d);
+        if (smem <= (small ? 48 : 200) * 1024) {
+            Real* C = static_cast<Real*>(out);
+            bool async_alloc = false;
+            if (U > 1) {
+                cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+                cudaStreamIsCapturing(s, &cap);
+                C = static_cast<Real*>(segment_scratch(dev, s, 23, sizeof(Real) * B * U * D,
+                                                       cap != cudaStreamCaptureStatusNone, &async_alloc));
+                if (!C) return cudaErrorMemoryAllocation;
+            }
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(B * U));
+            cfg.blockDim = dim3(small ? (unsigned)((D + 31) / 32 * 32) : 1024u);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaError_t e = cudaSuccess;
+            if (!small && smem > 48 * 1024)
+                e = cudaFuncSetAttribute(generic_walk_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+            if (e == cudaSuccess)
+                e = !small ? cudaLaunchKernelEx(&cfg, generic_walk_kernel<Real>, static_cast<const Real*>(X), L, d, N, D,
+                                                static_cast<Real*>(nullptr), U, CL, static_cast<const Real*>(nullptr), C)
+                    : N <= 4 ? cudaLaunchKernelEx(&cfg, generic_stream_small_kernel<Real, 4>,
+                                                  static_cast<const Real*>(X), L, d, N, D, static_cast<Real*>(nullptr),
+                                                  U, CL, static_cast<const Real*>(nullptr), C)
+                             : cudaLaunchKernelEx(&cfg, generic_stream_small_kernel<Real, 8>,
+                                                  static_cast<const Real*>(X), L, d, N, D, static_cast<Real*>(nullptr),
+                                                  U, CL, static_cast<const Real*>(nullptr), C);
+            if (e == cudaSuccess && U > 1) {
+                const size_t psm = 2 * sizeof(Real) * D;
+                if (psm > 48 * 1024)
+                    e = cudaFuncSetAttribute(chunk_product_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)psm);
+                if (e == cudaSuccess)
+                    chunk_product_kernel<Real><<<(unsigned)B, 256, psm, s>>>(C, D, d, N, U, static_cast<Real*>(out));
+            }
+            if (async_alloc) cudaFreeAsync(C, s);
+            return e == cudaSuccess ? cudaGetLastError() : e;
+        }
+    }
     generic_fold_kernel<Real><<<(unsigned)B, 256, sizeof(Real) * d, s>>>(static_cast<const Real*>(X), L, d, N, D,
                                                                           static_cast<Real*>(out));
     return cudaGetLastError();
@@ -1768,9 +1821,23 @@ static cudaError_t gen_stream(const void* X, int64_t B, int64_t L, int d, int N,
         cfg.dynamicSmemBytes = small_smem;
         if (N <= 4)
             return cudaLaunchKernelEx(&cfg, generic_stream_small_kernel<Real, 4>, static_cast<const Real*>(X), L, d, N,
-                                      D, static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts));
+                                      D, static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts),
+                                      static_cast<Real*>(nullptr));
         return cudaLaunchKernelEx(&cfg, generic_stream_small_kernel<Real, 8>, static_cast<const Real*>(X), L, d, N, D,
-                                  static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts));
+                                  static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts),
+                                  static_cast<Real*>(nullptr));
+    }
+    if (d <= 16 && small_smem <= 200 * 1024) {  // rows + points in shared memory, entries strided over 1024 threads
+        cfg.blockDim = dim3(1024);
+        cfg.dynamicSmemBytes = small_smem;
+        cudaError_t e = small_smem > 48 * 1024 ? cudaFuncSetAttribute(generic_walk_kernel<Real>,
+                                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                                      (int)small_smem)
+                                               : cudaSuccess;
+        if (e != cudaSuccess) return e;
+        return cudaLaunchKernelEx(&cfg, generic_walk_kernel<Real>, static_cast<const Real*>(X), L, d, N, D,
+                                  static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts),
+                                  static_cast<Real*>(nullptr));
     }
     return cudaLaunchKernelEx(&cfg, generic_stream_kernel<Real>, static_cast<const Real*>(X), L, d, N, D,
                               static_cast<Real*>(out), U, CL, static_cast<const Real*>(starts));

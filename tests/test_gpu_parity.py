@@ -276,3 +276,20 @@ def test_input_produced_by_previous_call_is_serialised(sk):
     X2 = out1.cpu().numpy().reshape(64, 13, 3).astype(np.float64)
     assert max(level_errors(out1.cpu().numpy(), ref1, 3, 3)) <= F32_TOL
     assert max(level_errors(out2.cpu().numpy(), O.signature(X2, 3), 3, 3)) <= F32_TOL
+
+
+@pytest.mark.parametrize("B,L,d,N", [(6, 1000, 9, 3), (4, 500, 3, 7), (3, 1500, 2, 9), (8, 700, 12, 2), (5, 300, 5, 4)])
+def test_generic_chunk_parallel_long_paths(sk, B, L, d, N):
+    # shapes without a register-sliced variant (and the forced generic family):
+    # chunk-parallel walks + the fixed-order product of the chunk signatures
+    X = brownian(B, L, d, seed=L + d)
+    ref = O.signature(X, N, threads=THREADS)
+    st = sk.KernelStats()
+    got = sk.signature_generic(X, N, stats=st)
+    assert max(level_errors(got, ref, d, N)) <= F64_TOL
+    X32 = X.astype(np.float32)
+    ref32 = O.signature(X32.astype(np.float64), N, threads=THREADS)
+    assert max(level_errors(sk.signature_generic(X32, N), ref32, d, N)) <= F32_TOL
+    rows = sk.signature_stream(X, N, family=sk.FAMILY_GENERIC)
+    _, ref_rows = O.signature(X[:2], N, stream=True)
+    assert np.max(np.abs(rows[:2] - ref_rows)) <= 1e-12 * np.max(np.abs(ref_rows))
