@@ -784,7 +784,22 @@ struct PairGeom {
     int* flags = nullptr;
     int epoch = 0;
     int segrow_off = 0;  // cluster launches: byte offset of the segment row in shared memory
+    int64_t sub_U = 0, sub_CL = 0, sub_L = 0;  // chunk paths (PairLaunch::sub_U)
 };
+
+// Path `b` of a pair-family launch: its points and step count (chunk paths:
+// a run of sub_CL + 1 points inside a path of X, shorter at the path's end).
+__device__ __forceinline__ const float* pair_path(const float* X, int64_t L, int d, const PairGeom& g, int64_t b,
+                                                  int64_t* M) {
+    if (g.sub_U > 0) {
+        const int64_t p = b / g.sub_U, j = b - (b / g.sub_U) * g.sub_U;
+        const int64_t s0 = j * g.sub_CL, left = g.sub_L - 1 - s0;
+        *M = left < g.sub_CL ? (left > 0 ? left : 0) : g.sub_CL;
+        return X + (p * g.sub_L + (s0 < g.sub_L ? s0 : g.sub_L - 1)) * d;
+    }
+    *M = L - 1;
+    return X + b * L * d;
+}
 
 // Offset of the cluster path's segment row (past every other use of the buffer).
 template <int d, int N, int Q>
@@ -908,12 +923,12 @@ __global__ void __launch_bounds__(NT, MINB) pair_kernel(const float* __restrict_
 
     const int64_t rowid = blockIdx.x;
     const int64_t b = rowid / g.G, sg = rowid - b * g.G;
-    const int64_t M = L - 1;
+    int64_t M;
+    const float* __restrict__ xb = pair_path(X, L, d, g, b, &M);
     const int64_t seg0 = sg * g.SL < M ? sg * g.SL : M;
     const int64_t slen = (seg0 + g.SL < M ? seg0 + g.SL : M) - seg0;
     const int U = g.U, UP = g.UP, CL = g.CL;
     const int tid = threadIdx.x, nth = blockDim.x;
-    const float* __restrict__ xb = X + b * L * d;
 
     f2* tab = reinterpret_cast<f2*>(smem_raw);                                   // [CL][UP][RS]
     float* raw = reinterpret_cast<float*>(smem_raw + (size_t)CL * UP * RS * 8);  // [(slen+1)*d + 4]

@@ -427,9 +427,17 @@ static int64_t covered_steps(int64_t M, int64_t G, int64_t U) {
     return n;
 }
 
+// Chunk paths (reverse mode): run_device's B paths of L = CL + 1 points are the
+// chunks of a (B / U, Lsrc, d) batch (PairLaunch::sub_U), read in place by the
+// pair family; other plans return kNeedGather without launching.
+struct SubPaths {
+    int64_t U = 0, CL = 0, Lsrc = 0;
+};
+constexpr int kNeedGather = -1000;
+
 template <typename Real>
 static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* out, cudaStream_t s,
-                      const sigk_tuning* tun, sigk_stats* st) {
+                      const sigk_tuning* tun, sigk_stats* st, const SubPaths* sub = nullptr) {
     const bool is_f64 = sizeof(Real) == 8;
     const int64_t D = [&] {
         int64_t t = 0, p = 1;
@@ -467,6 +475,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
     if (!(tun && (tun->force_generic || tun->family == SIGK_FAMILY_GENERIC)))
         plan = cached_plan(d, N, is_f64, dev, plan_rows, M, D, tun);
     const Variant* v = plan.v;
+    if (sub && (v == nullptr || v->family != KernelFamily::Pair || plan.pos)) return kNeedGather;
     if (v == nullptr) {
         record(ev0);
         e = is_f64 ? launch_generic_f64(X, B, L, d, N, out, s) : launch_generic_f32(X, B, L, d, N, out, s);
@@ -492,7 +501,7 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         void* rows = nullptr;
         void* counters = nullptr;
         bool async_rows = false, async_ctr = false;
-        const bool cluster = G > 1 && G <= kMaxPairCluster && tun && tun->cluster;
+        const bool cluster = G > 1 && G <= kMaxPairCluster && tun && tun->cluster && !sub;
         if (G > 1 && !cluster) {
             if (cap == cudaStreamCaptureStatusNone) cudaStreamIsCapturing(s, &cap);
             const bool capt = cap == cudaStreamCaptureStatusActive;
@@ -502,6 +511,11 @@ static int run_device(const Real* X, int64_t B, int64_t L, int d, int N, Real* o
         }
         PairLaunch a{X, B, L, G, SL, U, CL, out, rows, counters, s, overlap, ev0, ev1,
                      cap == cudaStreamCaptureStatusActive, tun ? tun->phase_buf : nullptr, cluster, plan.pos};
+        if (sub) {
+            a.sub_U = sub->U;
+            a.sub_CL = sub->CL;
+            a.sub_L = sub->Lsrc;
+        }
         e = v->pair_launch(a);
         if (async_rows) cudaFreeAsync(rows, s);
         if (async_ctr) cudaFreeAsync(counters, s);
@@ -1346,23 +1360,37 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
             release();
             return cuda_fail(e, "vjp chunk allocation");
         }
-        segment_gather_kernel<Real><<<(unsigned)std::min<int64_t>(B * U, (int64_t)sms * 16), 128, 0, s>>>(X, B, L, d, U, CL, Xseg);
+        // chunk signatures: the forward kernels on the chunks as paths of CL + 1 points, read
+        // in place where the plan is the pair family, else gathered first
         sigk_stats cst{};
-        const int rc = run_device<Real>(Xseg, B * U, CL + 1, d, N, C, s, nullptr, &cst);
+        const SubPaths sub{U, CL, L};
+        int rc = getenv("SIGK_VJP_GATHER") ? kNeedGather : run_device<Real>(X, B * U, CL + 1, d, N, C, s, nullptr, &cst, &sub);
+        if (rc == kNeedGather) {
+            segment_gather_kernel<Real><<<(unsigned)std::min<int64_t>(B * U, (int64_t)sms * 16), 128, 0, s>>>(X, B, L, d, U, CL, Xseg);
+            launches += 1;
+            rc = run_device<Real>(Xseg, B * U, CL + 1, d, N, C, s, nullptr, &cst);
+        }
         if (rc != SIGK_OK) {
             release();
             return rc;
         }
         const size_t bsm = 3 * sizeof(Real) * (size_t)D;
         cbars = cb;
-        launches += 1 + cst.launches;
+        launches += cst.launches;
         if (sl.fn) {
             if ((e = alloc(reinterpret_cast<void**>(&ends), sizeof(Real) * B * U * D)) != cudaSuccess) {
                 release();
                 return cuda_fail(e, "vjp allocation");
             }
         }
-        if (sl.fn) {  // slice shapes: boundary and ends in one compile-time pass per path
+        const size_t ssm = ((size_t)U * D + (size_t)2 * U * (D - p) + D) * sizeof(Real);  // ScanPasses::smem (p = d^N)
+        if (sl.scan && !getenv("SIGK_VJP_SERIAL_PASSES") && ssm <= 220 * 1024) {
+            // slice shapes: both passes by degree, every chunk at once
+            if (ssm > 48 * 1024)
+                cudaFuncSetAttribute(sl.scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+            sl.scan<<<(unsigned)(2 * B), 512, ssm, s>>>(C, cot, U, 1, cb, ends, L, CL, grad);
+            launches += 1;
+        } else if (sl.fn) {  // slice shapes: boundary and ends in one compile-time pass per path
             const size_t rsm = (size_t)(U + 4) * D * sizeof(Real);
             const int resident = rsm <= 200 * 1024;
             const size_t psm = resident ? rsm : 6 * D * sizeof(Real);

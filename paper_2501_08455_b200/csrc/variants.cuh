@@ -168,7 +168,11 @@ struct PairVariant {
         g.phases = static_cast<long long*>(a.phases);
         g.counters = static_cast<int*>(a.counters);
         g.final_out = static_cast<float*>(a.out);
+        g.sub_U = a.sub_U;
+        g.sub_CL = a.sub_CL;
+        g.sub_L = a.sub_L;
         const bool cl = a.cluster && a.G > 1;
+        if (a.sub_U > 0 && a.pos) return cudaErrorInvalidValue;  // chunk paths: the table-fold kernel only
         if (a.pos) {  // position-table fold, producer warp
             if (!HAS_POS || g.threads > NFP) return cudaErrorInvalidValue;
             const size_t sm = psmem(a.U, a.SL, a.G, cl);

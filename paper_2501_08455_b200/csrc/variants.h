@@ -40,6 +40,10 @@ struct PairLaunch {
     void* phases;  // optional [B*G][8] int64 phase stamps
     bool cluster;  // G in [2, kMaxPairCluster]: cluster launch (no scratch, no counters)
     bool pos;      // position-table fold with a producer warp (ppair_kernel.cuh); U/2 * P <= 128
+    // chunk paths (reverse mode): when sub_U > 0, path r of the launch (B = B0 * sub_U rows) is
+    // chunk r % sub_U of path r / sub_U of X ((B0, sub_L, d)): points j*sub_CL .. min((j+1)*sub_CL,
+    // sub_L - 1); L is then sub_CL + 1 (the gather kernel's layout, without the gather)
+    int64_t sub_U = 0, sub_CL = 0, sub_L = 0;
 };
 
 struct Variant {

@@ -33,6 +33,7 @@ static void slice_case(int d, int N, VjpSlice<Real>& out) {
             out.fn = vjp_slice_kernel<Real, DD, NN, Q>;
             out.slots = SliceLayout<DD, NN, Q>::SLOTS;
             out.passes = vjp_chunk_passes_kernel<Real, DD, NN>;
+            out.scan = vjp_scan_passes_kernel<Real, DD, NN>;
         }
     }
 }

@@ -235,6 +235,9 @@ struct VjpSlice {
     int slots = 0;  // (path, chunk) items per warp
     // compile-time boundary + ends pass (vjp_chunk_passes_kernel); null: the runtime kernels
     void (*passes)(const Real*, const Real*, int, int, Real*, Real*, int64_t, int64_t, Real*) = nullptr;
+    // the same passes by degree, all chunks at once (vjp_scan_passes_kernel; 512 threads,
+    // (U D + 2 U DL + D) values of shared memory, DL = the signature size below level N)
+    void (*scan)(const Real*, const Real*, int, int, Real*, Real*, int64_t, int64_t, Real*) = nullptr;
 };
 VjpSlice<float> vjp_slice_for_f32(int d, int N);
 VjpSlice<double> vjp_slice_for_f64(int d, int N);

@@ -661,4 +661,158 @@ __global__ void __launch_bounds__(ChunkPasses<Real, d, N>::NT) vjp_chunk_passes_
     }
 }
 
+// The same two passes by degree, every chunk at once (round 2; the pass above
+// is U dependent Chen steps per path, ~1.9 us each on B200). With E^(j) =
+// C^(0) ⊠ ... ⊠ C^(j) (the ends rows) and T^(j) = C^(j+1) ⊠ ... ⊠ C^(U-1)
+// (T^(U-1) = 1), level n of either needs only levels < n of the other rows:
+//   E_n^(j) = E_n^(j-1) + C_n^(j) + Σ_{a=1}^{n-1} E_a^(j-1) ⊗ C_{n-a}^(j)
+//   T_n^(j) = T_n^(j+1) + C_n^(j+1) + Σ_{a=1}^{n-1} C_a^(j+1) ⊗ T_{n-a}^(j+1)
+// (tensor_algebra.cpp:80-102). Per level two barrier-separated phases: the
+// increments (every (chunk, entry) independent), then the running sums over
+// the chunks (one thread per entry; its loads are independent of the sum).
+// Then the cotangent at every chunk end is the output cotangent pulled back
+// through right multiplication by T^(j) (the composition of the per-chunk
+// pull-backs the pass above applies one at a time):
+//   cbar^(j)_m[I] = cot_m[I] + Σ_{k=1}^{N-m} Σ_J cot_{m+k}[I·J] T_k^(j)[J].
+// Two CTAs per path (the forward and the backward scan run concurrently).
+// Shared memory (ScanPasses::smem): the C rows, levels < N of the E and T
+// rows and the cotangent; the level-N increments of E replace C_N in place and
+// their sums go straight to the ends rows (T_N is never needed).
+template <typename Real, int d, int N>
+struct ScanPasses {
+    static constexpr int D = level_off(d, N), DL = level_off(d, N - 1);
+    static constexpr int NT = 512;
+    __host__ __device__ static constexpr size_t smem(int U) { return ((size_t)U * D + (size_t)2 * U * DL + D) * sizeof(Real); }
+};
+
+template <typename Real, int d, int N>
+__global__ void __launch_bounds__(ScanPasses<Real, d, N>::NT) vjp_scan_passes_kernel(
+    const Real* __restrict__ C, const Real* __restrict__ cot, int U, int, Real* __restrict__ cbars,
+    Real* __restrict__ ends, int64_t L, int64_t CL, Real* __restrict__ grad) {
+    using SP = ScanPasses<Real, d, N>;
+    constexpr int D = SP::D, DL = SP::DL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Real* Cs = reinterpret_cast<Real*>(smem_raw);  // [U][D]  C^(j)
+    Real* Es = Cs + (size_t)U * D;                   // [U][DL] E^(j), levels < N
+    Real* Ts = Es + (size_t)U * DL;                  // [U][DL] T^(j), levels < N
+    Real* cs = Ts + (size_t)U * DL;                  // [D] output cotangent
+    // two CTAs per path: even blocks run the forward scan (E, the ends rows; they also zero
+    // the gradient's shared chunk points), odd blocks the backward scan (T, then the cbar rows)
+    const bool fwd = (blockIdx.x & 1) == 0;
+    const int64_t b = blockIdx.x >> 1;
+    const int tid = threadIdx.x;
+    const Real* Cb = C + b * U * D;
+    Real* eb = ends + b * U * D;
+    pdl_trigger();
+    pdl_wait();
+    if (fwd) {
+        Real* gb = grad + b * L * d;
+        for (int i = tid; i < (U - 1) * d; i += SP::NT) {
+            const int j = i / d;
+            gb[(int64_t)(j + 1) * CL * d + (i - j * d)] = Real(0);
+        }
+    }
+    // the predecessor's rows through L2 (ld.global.cg), 16-byte loads when aligned
+    if ((((size_t)U * D * sizeof(Real)) & 15) == 0 && (reinterpret_cast<uintptr_t>(Cb) & 15) == 0) {
+        const int4* src = reinterpret_cast<const int4*>(Cb);
+        int4* dst = reinterpret_cast<int4*>(Cs);
+        const int n16 = (int)((size_t)U * D * sizeof(Real) / 16);
+#pragma unroll 4
+        for (int i = tid; i < n16; i += SP::NT) dst[i] = __ldcg(src + i);
+    } else {
+#pragma unroll 4
+        for (int i = tid; i < U * D; i += SP::NT) Cs[i] = __ldcg(Cb + i);
+    }
+    if (!fwd)
+        for (int i = tid; i < D; i += SP::NT) cs[i] = __ldcg(cot + b * D + i);
+    __syncthreads();
+#pragma unroll
+    for (int n = 1; n <= N; ++n) {
+        if (!fwd && n == N) break;  // T_N is never needed
+        const int sz = ipow(d, n), on = level_off(d, n - 1);
+        // phase 1: increments. E: x^(j) = C_n^(j) + Σ_a E_a^(j-1) ⊗ C_{n-a}^(j) -> level n of
+        // E row j (of C row j for level N); T: y^(j) = C_n^(j+1) + Σ_a C_a^(j+1) ⊗
+        // T_{n-a}^(j+1) -> level n of T row j (row U-1: 0)
+        for (int w = tid; w < U * sz; w += SP::NT) {
+            const int j = w / sz, I = w - (w / sz) * sz;
+            if (fwd) {
+                Real x = Cs[(size_t)j * D + on + I];
+                if (j > 0) {
+#pragma unroll
+                    for (int a = 1; a < n; ++a) {
+                        const int tail = ipow(d, n - a);
+                        x = fma(Es[(size_t)(j - 1) * DL + level_off(d, a - 1) + I / tail],
+                                Cs[(size_t)j * D + level_off(d, n - a - 1) + I % tail], x);
+                    }
+                }
+                if (n < N) Es[(size_t)j * DL + on + I] = x;
+                else Cs[(size_t)j * D + on + I] = x;  // in place: no other item reads C_N^(j)[I]
+            } else {
+                Real y = Real(0);
+                if (j < U - 1) {
+                    y = Cs[(size_t)(j + 1) * D + on + I];
+#pragma unroll
+                    for (int a = 1; a < n; ++a) {
+                        const int tail = ipow(d, n - a);
+                        y = fma(Cs[(size_t)(j + 1) * D + level_off(d, a - 1) + I / tail],
+                                Ts[(size_t)(j + 1) * DL + level_off(d, n - a - 1) + I % tail], y);
+                    }
+                }
+                Ts[(size_t)j * DL + on + I] = y;
+            }
+        }
+        __syncthreads();
+        // phase 2: running sums over the chunks (E forwards, T backwards); the ends rows
+        for (int I = tid; I < sz; I += SP::NT) {
+            Real run = Real(0);
+            if (fwd && n < N) {
+                Real* e = Es + on + I;
+                Real* g = eb + on + I;
+                for (int j = 0; j < U; ++j) {
+                    run += e[(size_t)j * DL];
+                    e[(size_t)j * DL] = run;
+                    g[(size_t)j * D] = run;
+                }
+            } else if (fwd) {  // level N: the increments sit in the C rows
+                const Real* e = Cs + on + I;
+                Real* g = eb + on + I;
+                for (int j = 0; j < U; ++j) {
+                    run += e[(size_t)j * D];
+                    g[(size_t)j * D] = run;
+                }
+            } else {
+                Real* t = Ts + on + I;
+                for (int j = U - 1; j >= 0; --j) {
+                    run += t[(size_t)j * DL];
+                    t[(size_t)j * DL] = run;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (fwd) return;
+    // cbar rows, level by level (compile-time index structure; four partial sums:
+    // the level-1 entries carry ~D terms)
+    Real* cb = cbars + b * U * D;
+#pragma unroll
+    for (int m = 1; m <= N; ++m) {
+        const int sz = ipow(d, m), om = level_off(d, m - 1);
+        for (int w = tid; w < U * sz; w += SP::NT) {
+            const int j = w / sz, I = w - (w / sz) * sz;
+            Real acc[4] = {cs[om + I], Real(0), Real(0), Real(0)};
+            if (j < U - 1) {
+                const Real* tj = Ts + (size_t)j * DL;
+#pragma unroll
+                for (int k = 1; k <= N - m; ++k) {
+                    const Real* cr = cs + level_off(d, m + k - 1) + I * ipow(d, k);
+                    const Real* tr = tj + level_off(d, k - 1);
+#pragma unroll 16
+                    for (int J = 0; J < ipow(d, k); ++J) acc[J & 3] = fma(cr[J], tr[J], acc[J & 3]);
+                }
+            }
+            cb[(size_t)j * D + om + I] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        }
+    }
+}
+
 }  // namespace sigk
