@@ -10,7 +10,9 @@ for lib in "$@"; do
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
-        j=json.loads(l); print('$lib $shp', round(j['ms_per_step']*1e3,3), 'us frac', round(j['roofline']['frac'],4), j['config'].get('chunks'), j['config'].get('segments'))"
+        j=json.loads(l); sc=j['roofline'].get('single_call',{}); sp=sc.get('device_span_ms',{})
+        print('$lib $shp', round(j['ms_per_step']*1e3,3), 'us frac', round(j['roofline']['frac'],4), j['config'].get('chunks'), j['config'].get('segments'),
+              'span_us', {k: round(v*1e3,2) for k,v in sp.items()})"
   done
 done
 done
