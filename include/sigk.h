@@ -24,6 +24,9 @@
  *   sigk_signature_vjp_f32/_f64
  *                         ← sigkit::signature_vjp  include/sigkit/autodiff.hpp:35-38,
  *                           src/autodiff.cpp:31-107, 218-224 (reverse mode)
+ *   sigk_signature_vjp_parallel_f32/_f64
+ *                         ← sigkit::signature_vjp with KernelKind::Parallel (vjp_parallel,
+ *                           src/autodiff.cpp:108-214: the adjoint of the scan passes)
  *   sigk_signature_sharded_f32/_f64
  *                         ← signature() over a batch split across GPUs (rows are independent,
  *                           SPEC.md:220-221; tests/test_kernels.cpp:252-263)
@@ -191,6 +194,15 @@ int sigk_signature_vjp_f32(const float* X, size_t B, size_t L, int d, int N, con
                            unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats);
 int sigk_signature_vjp_f64(const double* X, size_t B, size_t L, int d, int N, const double* cotangent, double* grad,
                            unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats);
+/* Reverse mode of the parallel formulation (KernelKind::Parallel): the
+ * adjoint of the per-degree scan passes, the reference's vjp_parallel
+ * (src/autodiff.cpp:108-214), run as GPU suffix scans and per-position
+ * contractions over (B, L-1, D) workspaces; memory_cap as for
+ * sigk_signature_parallel_*. Same buffers and flags as sigk_signature_vjp_*. */
+int sigk_signature_vjp_parallel_f32(const float* X, size_t B, size_t L, int d, int N, const float* cotangent, float* grad,
+                                    size_t memory_cap, unsigned flags, void* stream, sigk_stats* stats);
+int sigk_signature_vjp_parallel_f64(const double* X, size_t B, size_t L, int d, int N, const double* cotangent,
+                                    double* grad, size_t memory_cap, unsigned flags, void* stream, sigk_stats* stats);
 
 /* Host buffers in and out; rows [g*ceil(B/G), ...) run on device g, one host
  * thread per device, each shard copied in, folded and copied back into its

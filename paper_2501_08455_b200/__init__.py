@@ -151,6 +151,8 @@ def lib():
                                       C.POINTER(_Stats)]
         for n in ("sigk_signature_parallel_f32", "sigk_signature_parallel_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, sz, C.c_uint, vp, C.POINTER(_Stats)]
+        for n in ("sigk_signature_vjp_parallel_f32", "sigk_signature_vjp_parallel_f64"):
+            getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, vp, sz, C.c_uint, vp, C.POINTER(_Stats)]
         for n in ("sigk_signature_vjp_f32", "sigk_signature_vjp_f64"):
             getattr(L, n).argtypes = [vp, sz, sz, C.c_int, C.c_int, vp, vp, C.c_uint, vp, C.POINTER(_Tuning),
                                       C.POINTER(_Stats)]
@@ -431,11 +433,21 @@ def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.
     """Reference ``sigkit::signature_vjp`` (autodiff.cpp:218-224): d<cotangent, Sig(X)>/dX,
     (B, L, d), for a (B, D) cotangent. numpy in -> numpy out; CUDA tensors in -> CUDA tensor out.
     ``chunks`` pins the number of backward chunks per path (0: planned; 1: one sequential walk).
-    Both kernel kinds run the same GPU adjoint (the reference's two adjoints agree,
-    test_autodiff.cpp:117-130)."""
-    select_kernel(kernel, caps or ExecutionCaps.detect(), _seq_len(paths))
+    As the reference, the selected kind picks the adjoint: Parallel runs the adjoint of the
+    per-degree scan passes (vjp_parallel, autodiff.cpp:108-214; sigk_signature_vjp_parallel_*,
+    with the forward formulation's storage cap), otherwise the fold adjoint (vjp_sequential,
+    :31-107). The two are independent GPU routes to the same gradient (test_autodiff.cpp:117-130)."""
+    kind = select_kernel(kernel, caps or ExecutionCaps.detect(), _seq_len(paths))
     st = _Stats()
     tun = C.byref(_Tuning(chunks=chunks)) if chunks else None
+    par = kind == KernelKind.Parallel
+
+    def call(fn32, fn64, is32, *a):
+        if par:
+            fn = lib().sigk_signature_vjp_parallel_f32 if is32 else lib().sigk_signature_vjp_parallel_f64
+            xp, B_, L_, d_, n_, cp, gp, flags, s = a
+            return fn(xp, B_, L_, d_, n_, cp, gp, DEFAULT_PARALLEL_MEMORY_CAP, flags, s, C.byref(st))
+        return (fn32 if is32 else fn64)(*a, tun, C.byref(st))
     if _is_torch(paths):
         import torch
 
@@ -448,19 +460,18 @@ def signature_vjp(paths, depth: int, cotangent, kernel: KernelKind = KernelKind.
         if tuple(cot.shape) != (B, sig_dim(d, depth)):
             raise DomainError("signature_vjp: cotangent shape does not match paths/depth")
         grad = torch.empty_like(X)
-        fn = lib().sigk_signature_vjp_f32 if X.dtype == torch.float32 else lib().sigk_signature_vjp_f64
         with torch.cuda.device(X.device):
             s = torch.cuda.current_stream(X.device).cuda_stream
-            _check(fn(X.data_ptr(), B, L, d, depth, cot.data_ptr(), grad.data_ptr(), SIGK_X_ON_DEVICE, s, tun,
-                      C.byref(st)))
+            _check(call(lib().sigk_signature_vjp_f32, lib().sigk_signature_vjp_f64, X.dtype == torch.float32,
+                        X.data_ptr(), B, L, d, depth, cot.data_ptr(), grad.data_ptr(), SIGK_X_ON_DEVICE, s))
     else:
         X, B, L, d = _host_array(paths, depth)
         cot = np.ascontiguousarray(cotangent, dtype=X.dtype)
         if cot.shape != (B, sig_dim(d, depth)):
             raise DomainError("signature_vjp: cotangent shape does not match paths/depth")
         grad = np.empty_like(X)
-        fn = lib().sigk_signature_vjp_f32 if X.dtype == np.float32 else lib().sigk_signature_vjp_f64
-        _check(fn(X.ctypes.data, B, L, d, depth, cot.ctypes.data, grad.ctypes.data, 0, None, tun, C.byref(st)))
+        _check(call(lib().sigk_signature_vjp_f32, lib().sigk_signature_vjp_f64, X.dtype == np.float32,
+                    X.ctypes.data, B, L, d, depth, cot.ctypes.data, grad.ctypes.data, 0, None))
     _copy_stats(st, stats)
     return grad
 

@@ -21,6 +21,7 @@
 #include "increments.cuh"
 #include "bruteforce.cuh"
 #include "scan_kernel.cuh"
+#include "scan_vjp.cuh"
 
 namespace sigk {
 
@@ -1488,9 +1489,110 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     return SIGK_OK;
 }
 
+// Reverse mode of the parallel formulation (KernelKind::Parallel; the
+// reference's vjp_parallel, autodiff.cpp:108-214): the forward scan passes
+// materialise every level (scan_kernel.cuh), then per degree n = N..1 a
+// suffix scan of the level cotangents and the cross-term distribution, the
+// diagonal chain per position and the point gradient (scan_vjp.cuh).
+static inline cudaStream_t s_of(void* stream) { return static_cast<cudaStream_t>(stream); }
+
+template <typename Real>
+static int vjp_parallel_device(const Real* X, int64_t B, int64_t L, int d, int N, const Real* cot, Real* grad,
+                               cudaStream_t s, sigk_stats* st) {
+    int64_t D = 0, p = 1;
+    for (int n = 0; n < N; ++n) {
+        p *= d;
+        D += p;
+    }
+    const int64_t M = L - 1;
+    sigk_stats local{};
+    local.family = SIGK_FAMILY_SCAN;
+    local.chunks = 1;
+    local.segments = 1;
+    local.prefix_len = -1;
+    cudaError_t e;
+    if (M == 0) {  // identity signature: zero gradient
+        e = cudaMemsetAsync(grad, 0, sizeof(Real) * B * L * d, s);
+        if (e != cudaSuccess) return cuda_fail(e, "memset");
+        local.scan_passes = N;
+        if (st) *st = local;
+        return SIGK_OK;
+    }
+    const size_t big = sizeof(Real) * (size_t)(B * M * D);
+    Real *W = nullptr, *Tb = nullptr, *Db = nullptr, *dbar = nullptr;
+    e = cudaMallocAsync(&W, big, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&Tb, big, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&Db, big, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&dbar, sizeof(Real) * (size_t)(B * M * d), s);
+    auto release = [&] {
+        for (Real* q : {W, Tb, Db, dbar})
+            if (q) cudaFreeAsync(q, s);
+    };
+    if (e != cudaSuccess) {
+        release();
+        return cuda_fail(e, "parallel reverse-mode workspace");
+    }
+    sigk_stats fst{};
+    int rc = parallel_device<Real>(X, B, L, d, N, W, true, s, &fst);  // every level at every position
+    if (rc != SIGK_OK) {
+        release();
+        return rc;
+    }
+    ScanGeom<Real> g{};
+    {
+        Real factorial = 1;
+        g.pw[0] = 1;
+        for (int j = 1; j <= N; ++j) {
+            g.pw[j] = g.pw[j - 1] * d;
+            factorial *= Real(j);
+            g.inv_fact[j] = Real(1) / factorial;
+            g.off[j] = g.off[j - 1] + g.pw[j];
+        }
+    }
+    e = cudaMemsetAsync(Tb, 0, big, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(Db, 0, big, s);
+    // seed: tbar[b, M-1] = cot[b] (every degree)
+    if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(Tb + (M - 1) * D, sizeof(Real) * M * D, cot, sizeof(Real) * D, sizeof(Real) * D, B,
+                              cudaMemcpyDeviceToDevice, s);
+    const int sms = device_info([] { int v = 0; cudaGetDevice(&v); return v; }()).sms;
+    int launches = fst.launches + 1;
+    constexpr int NW = 8;
+    for (int n = N; n >= 1 && e == cudaSuccess; --n) {
+        degree_suffix_kernel<Real, NW><<<(unsigned)(B * ((g.pw[n] + 31) / 32)), 32 * NW, 0, s>>>(n, M, Tb, Db, D, g);
+        launches += 1;
+        if (n >= 2 && M >= 2) {
+            const int64_t work = (M - 1) * 2 * g.off[n - 1];
+            const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)sms * 8));
+            degree_distribute_kernel<Real><<<dim3(gx, (unsigned)B), 256, 0, s>>>(X, L, d, n, M, W, Tb, Db, D, g);
+            launches += 1;
+        }
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+        const int64_t warps = B * M;
+        diag_chain_kernel<Real><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((warps + 3) / 4, (int64_t)sms * 16)), 128, 0, s>>>(
+            X, L, d, N, M, B, Db, D, dbar, g);
+        const int64_t ng = B * L * d;
+        vjp_grad_kernel<Real><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((ng + 255) / 256, (int64_t)sms * 16)), 256, 0, s>>>(
+            dbar, B, L, d, grad);
+        launches += 2;
+        e = cudaGetLastError();
+    }
+    release();
+    if (e != cudaSuccess) return cuda_fail(e, "parallel reverse mode");
+    local.scan_passes = 2 * N;  // the forward degree passes and the reverse ones
+    local.launches = launches;
+    local.path_steps = M;
+    local.fold_steps = 0;
+    if (st) *st = local;
+    return SIGK_OK;
+}
+
 template <typename Real>
 static int vjp_impl(const Real* X, size_t B, size_t L, int d, int N, const Real* cot, Real* grad, unsigned flags,
-                    void* stream, const sigk_tuning* tun, sigk_stats* st) {
+                    void* stream, const sigk_tuning* tun, sigk_stats* st, bool parallel = false,
+                    size_t memory_cap = 0) {
     g_err.clear();
     int rc = validate(X, B, L, d, N, grad);
     if (rc != SIGK_OK) return rc;
@@ -1505,13 +1607,25 @@ static int vjp_impl(const Real* X, size_t B, size_t L, int d, int N, const Real*
             return fail(SIGK_EDOMAIN, "signature_vjp: grad must not overlap the paths or the cotangent");
     }
     if (N > kGenericMaxDepth) return fail(SIGK_ERESOURCE, "signature_vjp: depth above 16 is not supported");
+    if (parallel) {  // the forward formulation's storage check (vjp_parallel runs parallel_forward first)
+        long double scalars = static_cast<long double>(B) * static_cast<long double>(L);
+        for (int n = 0; n < N; ++n) scalars *= static_cast<long double>(d);
+        if (scalars > static_cast<long double>(memory_cap))
+            return fail(SIGK_ERESOURCE, "parallel kernel: intermediate storage of ~" +
+                                            std::to_string(static_cast<double>(scalars)) + " scalars exceeds cap " +
+                                            std::to_string(memory_cap) + "; use the sequential kernel for this shape");
+    }
+    auto run = [&](const Real* x, const Real* c, Real* g_) {
+        return parallel ? vjp_parallel_device<Real>(x, (int64_t)B, (int64_t)L, d, N, c, g_, s_of(stream), st)
+                        : vjp_device<Real>(x, (int64_t)B, (int64_t)L, d, N, c, g_, s_of(stream), tun, st);
+    };
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     size_t D = 0;
     sigk_sig_dim(d, N, &D);
     const size_t xbytes = sizeof(Real) * B * L * d, cbytes = sizeof(Real) * B * D;
     cudaError_t e;
     if (flags & SIGK_X_ON_DEVICE) {
-        rc = vjp_device<Real>(X, (int64_t)B, (int64_t)L, d, N, cot, grad, s, tun, st);
+        rc = run(X, cot, grad);
         if (rc == SIGK_OK) {
             e = cudaPeekAtLastError();
             if (e != cudaSuccess) rc = cuda_fail(e, "kernel launch");
@@ -1539,7 +1653,7 @@ static int vjp_impl(const Real* X, size_t B, size_t L, int d, int N, const Real*
     Real* gd = reinterpret_cast<Real*>(base + goff);
     if ((e = cudaMemcpyAsync(xd, X, xbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D");
     if ((e = cudaMemcpyAsync(cd, cot, cbytes, cudaMemcpyHostToDevice, s)) != cudaSuccess) return cuda_fail(e, "H2D");
-    rc = vjp_device<Real>(xd, (int64_t)B, (int64_t)L, d, N, cd, gd, s, tun, st);
+    rc = run(xd, cd, gd);
     if (rc == SIGK_OK && (e = cudaMemcpyAsync(grad, gd, xbytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         rc = cuda_fail(e, "D2H");
     e = cudaStreamSynchronize(s);
@@ -1711,6 +1825,16 @@ int sigk_signature_vjp_f32(const float* X, size_t B, size_t L, int d, int N, con
 int sigk_signature_vjp_f64(const double* X, size_t B, size_t L, int d, int N, const double* cotangent, double* grad,
                            unsigned flags, void* stream, const sigk_tuning* tuning, sigk_stats* stats) {
     return sigk::vjp_impl<double>(X, B, L, d, N, cotangent, grad, flags, stream, tuning, stats);
+}
+
+int sigk_signature_vjp_parallel_f32(const float* X, size_t B, size_t L, int d, int N, const float* cotangent, float* grad,
+                                    size_t memory_cap, unsigned flags, void* stream, sigk_stats* stats) {
+    return sigk::vjp_impl<float>(X, B, L, d, N, cotangent, grad, flags, stream, nullptr, stats, true, memory_cap);
+}
+
+int sigk_signature_vjp_parallel_f64(const double* X, size_t B, size_t L, int d, int N, const double* cotangent,
+                                    double* grad, size_t memory_cap, unsigned flags, void* stream, sigk_stats* stats) {
+    return sigk::vjp_impl<double>(X, B, L, d, N, cotangent, grad, flags, stream, nullptr, stats, true, memory_cap);
 }
 
 int sigk_signature_sharded_f32(const float* X, size_t B, size_t L, int d, int N, float* out, int num_gpus,

@@ -94,14 +94,21 @@ PathGradient signature_vjp(const PathBatch& paths, int depth, const SignatureCot
         throw DomainError("signature_vjp: cotangent has " + std::to_string(cot.values.size()) + " values, expected " +
                           std::to_string(cot.batch * width));
     validate_paths(paths);
-    (void)select_kernel(kernel, caps, paths.len);
+    const KernelKind kind = select_kernel(kernel, caps, paths.len);
     PathGradient g;
     g.batch = paths.batch;
     g.len = paths.len;
     g.dim = paths.dim;
     g.values.assign(paths.values.size(), 0.0);
-    check(sigk_signature_vjp_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, cot.values.data(),
-                                 g.values.data(), 0u, nullptr, nullptr, nullptr));
+    // as the reference (autodiff.cpp:218-224): Parallel runs the adjoint of the scan passes
+    // (vjp_parallel, with parallel_forward's default storage cap), otherwise the fold adjoint
+    if (kind == KernelKind::Parallel)
+        check(sigk_signature_vjp_parallel_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth,
+                                              cot.values.data(), g.values.data(), kDefaultParallelMemoryCap, 0u,
+                                              nullptr, nullptr));
+    else
+        check(sigk_signature_vjp_f64(paths.values.data(), paths.batch, paths.len, paths.dim, depth, cot.values.data(),
+                                     g.values.data(), 0u, nullptr, nullptr, nullptr));
     return g;
 }
 

@@ -125,3 +125,54 @@ def test_segment_scratch_survives_growth_under_graph_replay(sk):
     assert max(level_errors(out.cpu().numpy(), ref, 5, 4)) <= 1e-5
     ref_big = O.signature(big.cpu().numpy().astype(np.float64)[:16], 4)
     assert max(level_errors(big_out.cpu().numpy()[:16], ref_big, 5, 4)) <= 1e-5
+
+
+# ---- reverse mode of the parallel formulation (KernelKind::Parallel -> vjp_parallel,
+# autodiff.cpp:108-214): GPU suffix scans + per-position contractions (scan_vjp.cuh)
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+@pytest.mark.parametrize("B,L,d,N", [(3, 2, 3, 3), (2, 9, 2, 4), (4, 33, 3, 4), (2, 40, 5, 3), (3, 17, 1, 5), (2, 12, 4, 1)])
+def test_parallel_vjp_matches_reference_vjp_parallel(sk, B, L, d, N):
+    X = brownian(B, L, d, seed=7 * L + d)
+    rng = np.random.default_rng(B + L)
+    cot = rng.standard_normal((B, sk.sig_dim(d, N)))
+    st = sk.KernelStats()
+    g = sk.signature_vjp(X, N, cot, kernel=sk.KernelKind.Parallel, stats=st)
+    assert st.family == sk.FAMILY_SCAN and st.scan_passes == 2 * N
+    if O.ref() is not None:
+        assert _rel(g, O.ref_vjp(X, N, cot, kernel="parallel")) <= 1e-12
+    # the two GPU adjoints agree (test_autodiff.cpp:117-130)
+    g_seq = sk.signature_vjp(X, N, cot, kernel=sk.KernelKind.Sequential)
+    assert _rel(g, g_seq) <= 1e-10
+
+
+def test_parallel_vjp_headline_shape_f32_and_device(sk):
+    torch = pytest.importorskip("torch")
+    X = brownian(32, 1000, 5, seed=3)
+    cot = np.random.default_rng(3).standard_normal((32, 780))
+    g64 = sk.signature_vjp(X, 4, cot, kernel=sk.KernelKind.Parallel)
+    g_seq = sk.signature_vjp(X, 4, cot, kernel=sk.KernelKind.Sequential)
+    assert _rel(g64, g_seq) <= 1e-10
+    Xt = torch.from_numpy(X.astype(np.float32)).cuda()
+    ct = torch.from_numpy(cot.astype(np.float32)).cuda()
+    g32 = sk.signature_vjp(Xt, 4, ct, kernel=sk.KernelKind.Parallel)
+    assert g32.is_cuda and g32.dtype == torch.float32
+    assert _rel(g32.cpu().numpy().astype(np.float64), g64) <= 1e-4
+
+
+def test_parallel_vjp_edges_and_cap(sk):
+    cot = np.ones((2, sk.sig_dim(3, 2)))
+    g = sk.signature_vjp(np.ones((2, 1, 3)), 2, cot, kernel=sk.KernelKind.Parallel)
+    assert g.shape == (2, 1, 3) and not g.any()
+    X = brownian(2, 2, 3, seed=5)  # one step: only the diagonal terms
+    if O.ref() is not None:
+        assert _rel(sk.signature_vjp(X, 2, cot, kernel=sk.KernelKind.Parallel), O.ref_vjp(X, 2, cot, kernel="parallel")) <= 1e-12
+    with pytest.raises(sk.ResourceError, match="exceeds cap 2147483648"):
+        sk.signature_vjp(np.zeros((64, 500, 10)), 5, np.zeros((64, sk.sig_dim(10, 5))), kernel=sk.KernelKind.Parallel)
+    # Auto follows the caps, like the forward
+    st = sk.KernelStats()
+    sk.signature_vjp(brownian(2, 80, 3), 3, np.ones((2, 39)), caps=sk.ExecutionCaps(accelerated=True), stats=st)
+    assert st.family == sk.FAMILY_SCAN

@@ -1,6 +1,7 @@
 #!/bin/bash
 # compute-sanitizer over the round-2 device paths: the parallel (per-degree scan)
-# formulation, the cluster (DSMEM) segment combine, the position-table fold with its
+# formulation and its reverse mode, the chunked reverse mode (in-place chunk
+# signatures, by-degree chunk passes), the cluster (DSMEM) segment combine, the position-table fold with its
 # producer warp (mbarrier pipeline), and the scratch-lifetime graph test.
 S=/usr/local/cuda/bin/compute-sanitizer
 cat > /tmp/san_r02.py <<'PY'
@@ -19,6 +20,14 @@ for kw in ({"segments": 2}, {"segments": 4, "chunks": 6}, {"segments": 8}, {"fol
 p = sk.signature_parallel(X.astype(np.float64), 4)
 assert np.abs(p - ref).max() < 1e-10
 rows = sk.signature_stream(X[:2].astype(np.float64), 3, kernel=sk.KernelKind.Parallel)
+# reverse modes: the parallel formulation's adjoint (scan_vjp.cuh) and the chunked fold adjoint
+# with in-place chunk signatures and the by-degree chunk passes
+cot = rng.standard_normal((3, 155))
+gp = sk.signature_vjp(X[:3].astype(np.float64), 3, cot, kernel=sk.KernelKind.Parallel)
+gs = sk.signature_vjp(X[:3].astype(np.float64), 3, cot, kernel=sk.KernelKind.Sequential)
+assert np.abs(gp - gs).max() <= 1e-10 * np.abs(gs).max()
+g32 = sk.signature_vjp(X[:3], 3, cot.astype(np.float32), chunks=6)
+assert np.abs(g32 - gs).max() <= 1e-4 * np.abs(gs).max()
 print("sanitized paths ok")
 PY
 for tool in memcheck racecheck synccheck; do
