@@ -302,20 +302,22 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
     const bool first_chunk = j == 0, last_chunk = j == U - 1;
     Real* gb = grad + b * L * d;
     Real prev = Real(0);  // δ̄_{s+1} of this lane's component
-    for (int64_t st = 0; st < CL; ++st) {
+    // past the chunk's start the point repeats (δ = 0, the identity step): the
+    // next point is loaded through a running pointer, or kept
+    const Real* xp = xb + (s_hi - 2) * d;  // X[s - 1] for the first step s = s_hi - 1
+    for (int64_t st = 0; st < CL; ++st, xp -= d) {
         const int64_t s = s_hi - 1 - st;
-        const bool on = valid && s >= s_lo;
         const bool pre_on = valid && s - 1 >= s_lo;
         Real xnx[d], pnx[Q + 1];
 #pragma unroll
-        for (int c = 0; c < d; ++c) xnx[c] = pre_on ? xb[(s - 1) * d + c] : Real(0);
+        for (int c = 0; c < d; ++c) xnx[c] = pre_on ? xp[c] : xlo[c];
 #pragma unroll
-        for (int k = 1; k <= Q; ++k) pnx[k] = pre_on ? xb[(s - 1) * d + dg[k]] : Real(0);
+        for (int k = 1; k <= Q; ++k) pnx[k] = pre_on ? xp[dg[k]] : plo[k];
         Real dl[d], dp[Q + 1];
 #pragma unroll
-        for (int c = 0; c < d; ++c) dl[c] = on ? xhi[c] - xlo[c] : Real(0);
+        for (int c = 0; c < d; ++c) dl[c] = xhi[c] - xlo[c];
 #pragma unroll
-        for (int k = 1; k <= Q; ++k) dp[k] = on ? phi[k] - plo[k] : Real(0);
+        for (int k = 1; k <= Q; ++k) dp[k] = phi[k] - plo[k];
 #pragma unroll
         for (int c = 0; c < d; ++c) {
             xhi[c] = xlo[c];
@@ -468,7 +470,7 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
                 rd[lane][c] = v;
             }
             __syncwarp();
-            if (on && p < d) {
+            if (valid && s >= s_lo && p < d) {
                 Real sum = Real(0);
                 for (int q = 0; q < P; ++q) sum += rd[slot * P + q][p];
                 if (st > 0) gb[(s + 1) * d + p] = sum - prev;
