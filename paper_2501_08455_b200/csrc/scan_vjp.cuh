@@ -31,15 +31,16 @@
 namespace sigk {
 
 // δ_k^{⊗j}/j! at multi-index J (digits of J, last one fastest), on the fly
-// from the step's two points x0 = X[k], x1 = X[k+1].
+// from the step's two points x0 = X[k], x1 = X[k+1] (32-bit digit arithmetic:
+// every multi-index here is below the storage cap, 2^31).
 template <typename Real>
-__device__ __forceinline__ Real diag_entry(const Real* __restrict__ x0, const Real* __restrict__ x1, int d, int j,
-                                           int64_t J, Real inv_fact_j) {
+__device__ __forceinline__ Real diag_entry(const Real* __restrict__ x0, const Real* __restrict__ x1, unsigned d, int j,
+                                           unsigned J, Real inv_fact_j) {
     Real v = inv_fact_j;
     for (int r = 0; r < j; ++r) {
-        const int c = (int)(J % d);
+        const unsigned q = J / d, c = J - q * d;
         v *= x1[c] - x0[c];
-        J /= d;
+        J = q;
     }
     return v;
 }
@@ -74,9 +75,10 @@ __global__ void __launch_bounds__(32 * NW) degree_suffix_kernel(int n, int64_t M
     }
 }
 
-// Cross-term distribution of degree n (n >= 2). One thread per (position k >= 1,
-// output entry): outputs [0, DLn) are tbar_m[k-1] entries (levels m = 1..n-1 in
-// row order), [DLn, 2 DLn) the diagbar_j[k] entries (levels j = 1..n-1).
+// Cross-term distribution of degree n (n >= 2). One thread per (position
+// k >= 1, output entry) of path blockIdx.y: entries [0, DLn) of a position are
+// tbar_m[k-1] (levels m = 1..n-1 in row order), [DLn, 2 DLn) the diagbar_j[k]
+// entries (levels j = 1..n-1).
 template <typename Real>
 __global__ void __launch_bounds__(256) degree_distribute_kernel(const Real* __restrict__ X, int64_t L, int d, int n,
                                                                 int64_t M, const Real* __restrict__ W,
@@ -92,25 +94,27 @@ __global__ void __launch_bounds__(256) degree_distribute_kernel(const Real* __re
     const Real* wb = W + b * M * D;
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = 1 + w / per_pos;
-        int64_t e = w - (w / per_pos) * per_pos;
+        int64_t e = w - (k - 1) * per_pos;
         const bool right = e < DLn;  // tbar_m[k-1] (else diagbar_j[k])
         if (!right) e -= DLn;
         int lev = 1;
         while (e >= g.off[lev]) ++lev;  // level of the output entry
-        const int64_t idx = e - g.off[lev - 1];
+        const unsigned idx = (unsigned)(e - g.off[lev - 1]);
         const Real* x0 = xb + k * d;
         const Real* x1 = x0 + d;
         const Real* u = tb + k * D + g.off[n - 1];  // tbar_n[k]
         Real acc = 0;
         if (right) {  // m = lev, j = n - m: Σ_J u[I·d^j + J] diag_j[J]
             const int j = n - lev;
-            const Real* row = u + idx * g.pw[j];
-            for (int64_t J = 0; J < g.pw[j]; ++J) acc += row[J] * diag_entry(x0, x1, d, j, J, g.inv_fact[j]);
+            const unsigned pj = (unsigned)g.pw[j];
+            const Real* row = u + (int64_t)idx * pj;
+            for (unsigned J = 0; J < pj; ++J) acc += row[J] * diag_entry(x0, x1, (unsigned)d, j, J, g.inv_fact[j]);
             tb[(k - 1) * D + g.off[lev - 1] + idx] += acc;
         } else {  // j = lev, m = n - j: Σ_I u[I·d^j + J] T_m[k-1][I]
             const int j = lev, m = n - lev;
             const Real* tm = wb + (k - 1) * D + g.off[m - 1];
-            for (int64_t I = 0; I < g.pw[m]; ++I) acc += u[I * g.pw[j] + idx] * tm[I];
+            const unsigned pm = (unsigned)g.pw[m], pj = (unsigned)g.pw[j];
+            for (unsigned I = 0; I < pm; ++I) acc += u[(int64_t)I * pj + idx] * tm[I];
             db[k * D + g.off[j - 1] + idx] += acc;
         }
     }
@@ -118,10 +122,10 @@ __global__ void __launch_bounds__(256) degree_distribute_kernel(const Real* __re
 
 // diag_n = diag_{n-1} ⊗ δ / n reversed per position, n = N..2 (in place on the
 // Db row, autodiff.cpp:179-197), then δ̄ = diagbar_1 + the chain's δ terms ->
-// dbar (B, M, d). One warp per position: lanes split the prefixes I for
+// dbar (B, M, d). One warp per position, lanes over the prefixes I:
 //   dbp[I] += (1/n) Σ_c dbn[I·d + c] δ[c]
-// and the channels c for
-//   δ̄[c] += (1/n) Σ_I dbn[I·d + c] diag_{n-1}[I].
+//   δ̄[c]  += (1/n) Σ_I dbn[I·d + c] diag_{n-1}[I]   (per-lane partials, 8 channels
+//                                                    at a time, then a warp sum)
 template <typename Real>
 __global__ void __launch_bounds__(128) diag_chain_kernel(const Real* __restrict__ X, int64_t L, int d, int N, int64_t M,
                                                          int64_t B, Real* __restrict__ Db, int64_t D,
@@ -134,27 +138,41 @@ __global__ void __launch_bounds__(128) diag_chain_kernel(const Real* __restrict_
         const Real* x0 = X + (b * L + k) * d;
         const Real* x1 = x0 + d;
         Real* row = Db + pos * D;
-        for (int c = lane; c < d; c += 32) dbar[pos * d + c] = 0;
+        Real* out = dbar + pos * d;
+        for (int c = lane; c < d; c += 32) out[c] = 0;
+        __syncwarp();
         for (int n = N; n >= 2; --n) {
             const Real inv = Real(1) / Real(n);
             const Real* dbn = row + g.off[n - 1];
             Real* dbp = row + g.off[n - 2];
-            // δ̄ terms first: they read dbn only (dbp is level n-1, written below)
-            for (int c = lane; c < d; c += 32) {
-                Real a = 0;
-                for (int64_t I = 0; I < g.pw[n - 1]; ++I)
-                    a += dbn[I * d + c] * diag_entry(x0, x1, d, n - 1, I, g.inv_fact[n - 1]);
-                dbar[pos * d + c] += inv * a;
+            const unsigned pp = (unsigned)g.pw[n - 1];
+            // δ̄ terms (read dbn only; dbp is level n-1, updated below)
+            for (int c0 = 0; c0 < d; c0 += 8) {
+                Real part[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) part[q] = 0;
+                for (unsigned I = lane; I < pp; I += 32) {
+                    const Real dv = diag_entry(x0, x1, (unsigned)d, n - 1, I, g.inv_fact[n - 1]);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (c0 + q < d) part[q] += dbn[(int64_t)I * d + c0 + q] * dv;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    Real v = part[q];
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    if (lane == 0 && c0 + q < d) out[c0 + q] += inv * v;
+                }
             }
-            for (int64_t I = lane; I < g.pw[n - 1]; I += 32) {
+            for (unsigned I = lane; I < pp; I += 32) {
                 Real a = 0;
-                for (int c = 0; c < d; ++c) a += dbn[I * d + c] * (x1[c] - x0[c]);
+                for (int c = 0; c < d; ++c) a += dbn[(int64_t)I * d + c] * (x1[c] - x0[c]);
                 dbp[I] += inv * a;
             }
             __syncwarp();
         }
         // + diagbar_1 after the chain (the n = 2 step updated it; level 1 = the increments)
-        for (int c = lane; c < d; c += 32) dbar[pos * d + c] += row[c];
+        for (int c = lane; c < d; c += 32) out[c] += row[c];
         __syncwarp();
     }
 }

@@ -1173,7 +1173,7 @@ static int parallel_device(const Real* X, int64_t B, int64_t L, int d, int N, Re
         if (e != cudaSuccess) return cuda_fail(e, "parallel-formulation workspace");
         scratch = true;
     }
-    constexpr int NW = 8;
+    constexpr int NW = 32;  // 32 ranges of the sequence per (path, 32-entry tile): shorter serial walks
     for (int n = 1; n <= N && e == cudaSuccess; ++n) {
         const int64_t grid = B * ((g.pw[n] + 31) / 32);
         if (N <= 8) degree_scan_kernel<Real, NW, 8><<<(unsigned)grid, 32 * NW, 0, s>>>(X, L, d, n, M, W, D, g);
@@ -1557,7 +1557,7 @@ static int vjp_parallel_device(const Real* X, int64_t B, int64_t L, int d, int N
                               cudaMemcpyDeviceToDevice, s);
     const int sms = device_info([] { int v = 0; cudaGetDevice(&v); return v; }()).sms;
     int launches = fst.launches + 1;
-    constexpr int NW = 8;
+    constexpr int NW = 32;  // 32 ranges of the sequence per (path, 32-entry tile): shorter serial walks
     for (int n = N; n >= 1 && e == cudaSuccess; --n) {
         degree_suffix_kernel<Real, NW><<<(unsigned)(B * ((g.pw[n] + 31) / 32)), 32 * NW, 0, s>>>(n, M, Tb, Db, D, g);
         launches += 1;
