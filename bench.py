@@ -188,10 +188,19 @@ def bind_to_gpu_numa(index):
     return None
 
 
+# SIGK_BENCH_SHARE_GPU=1 (plumbing checks on a one-GPU box, never a bench value): ranks
+# share the visible GPUs round robin and talk over gloo (NCCL needs one GPU per rank)
+SHARE_GPU = bool(os.environ.get("SIGK_BENCH_SHARE_GPU"))
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARE_GPU:
+        import torch
+
+        local %= max(1, torch.cuda.device_count())
     return rank, world, local
 
 
@@ -201,7 +210,7 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARE_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -283,7 +292,10 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     _, L, d, N = CONFIGS[args.config]
     B_global, row0, B, scaling = rank_rows(args.config, world, rank)
