@@ -26,7 +26,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
            "-I" + os.path.join(ROOT, "include"), "-I" + CSRC] + DEFS
 DIMS = [1, 2, 3, 4, 5, 6, 7, 8, 10]
-HEADERS = ["sigk_common.cuh", "fold.cuh", "merge.cuh", "pair_kernel.cuh", "ipair_kernel.cuh", "stream_kernel.cuh", "vjp_kernel.cuh", "vjp_slice.cuh", "increments.cuh", "scan_kernel.cuh", "pos_fold.cuh", "ppair_kernel.cuh", "generic.cuh", "variants.cuh", "variants.h"]
+HEADERS = ["sigk_common.cuh", "fold.cuh", "merge.cuh", "pair_kernel.cuh", "ipair_kernel.cuh", "stream_kernel.cuh", "vjp_kernel.cuh", "vjp_slice.cuh", "increments.cuh", "scan_kernel.cuh", "scan_vjp.cuh", "vjp_prep.cuh", "pos_fold.cuh", "ppair_kernel.cuh", "generic.cuh", "variants.cuh", "variants.h"]
 
 
 def _units():

@@ -431,6 +431,12 @@ static int64_t covered_steps(int64_t M, int64_t G, int64_t U) {
 // Chunk paths (reverse mode): run_device's B paths of L = CL + 1 points are the
 // chunks of a (B / U, Lsrc, d) batch (PairLaunch::sub_U), read in place by the
 // pair family; other plans return kNeedGather without launching.
+// reverse mode: the longest chunk one fold-and-passes CTA takes (longer paths chunk
+// over more CTAs: chunk signatures in place, then the pass kernel)
+constexpr int64_t kPrepMaxChunkSteps = 160;
+constexpr int kPrepMaxChunks = 20;  // the passes walk the chunks serially per entry
+constexpr int64_t kPrepMinSteps = 750;
+
 struct SubPaths {
     int64_t U = 0, CL = 0, Lsrc = 0;
 };
@@ -1333,12 +1339,70 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         }
         if (tun && tun->chunks > 1) U = (int)std::min<int64_t>(tun->chunks, M);
     }
-    const int64_t CL = M > 0 ? (M + U - 1) / U : 1;
+    // fp32 shapes with a pair variant and a slice walk, paths short enough to fold in one
+    // CTA: one launch folds every path's U chunks and runs both chunk passes in shared
+    // memory (vjp_prep.cuh), replacing the chunk-signature launch, its rows and the pass
+    // launch. The walk's time does not depend on the chunk count (C2: 55.6 / 53.0 /
+    // 54.6 us at U = 9 / 18 / 36), so U is the CTA's widest chunking.
+    const Variant* prep = nullptr;
+    int prepU = 0;
+    int64_t prepCL = 0;
+    if constexpr (sizeof(Real) == 4) {
+        // one fold-and-passes CTA per path and SM (~160 registers x 256 threads): only
+        // batches that fit one wave (B = 1024, L = 200 measured 263 vs 80 us otherwise),
+        // and paths long enough that the launches it saves outweigh its serial passes
+        // (measured: 72 vs 76 us at 128 x 1000, 69 vs 74 at 32 x 2000; 29 vs 25 at
+        // 16 x 500 (d 2, N 6), 23 vs 21 at 64 x 300 (d 4, N 4))
+        if (sl.fn && M >= kPrepMinSteps && B <= sms && !(tun && tun->chunks > 0) && !getenv("SIGK_VJP_NO_PREP")) {
+            const Variant* cands[8];
+            const int nc = find_variants(d, N, false, cands, 8);
+            for (int i = 0; i < nc; ++i) {
+                const Variant* v = cands[i];
+                if (v->family != KernelFamily::Pair || !v->vjp_prep_launch) continue;
+                // the fold CTA takes up to 2 * units_max chunks; among those chunkings pick the
+                // one the walk likes (its CTAs per SM x steps per chunk, the model of the
+                // chunk search above; ties: more chunks, a wider fold). C2: U = 18
+                // (576 walk CTAs = 4 per SM x 56 steps): 71.4 us vs 78.0 at U = 20 (5 x 50)
+                const int umax = std::min(2 * v->pair_units_max, kPrepMaxChunks);
+                int64_t best = -1;
+                int ub = 0;
+                for (int uc = 2; uc <= umax; uc += 2) {
+                    const int64_t cl = (M + uc - 1) / uc;
+                    if (cl > kPrepMaxChunkSteps || v->vjp_prep_smem(uc, (int)cl, L) > 227 * 1024) continue;
+                    const int64_t r = (M + cl - 1) / cl, ctas = (B * r + 4 * sl.slots - 1) / (4 * sl.slots);
+                    const int64_t cost = (ctas + sms - 1) / sms * cl;
+                    if (best < 0 || cost <= best) {
+                        best = cost;
+                        ub = uc;
+                    }
+                }
+                if (const char* f = getenv("SIGK_VJP_PREP_U")) ub = std::max(2, std::min(umax, atoi(f) / 2 * 2));  // experiments
+                if (ub == 0) continue;
+                prep = v;
+                prepU = ub;
+                prepCL = (M + ub - 1) / ub;
+                break;
+            }
+        }
+    }
+    if (prep) U = (int)((M + prepCL - 1) / prepCL);
+    const int64_t CL = prep ? prepCL : (M > 0 ? (M + U - 1) / U : 1);
     if (M > 0) U = (int)((M + CL - 1) / CL);
     int launches = 0;
     const Real* cbars = cot;
     Real* ends = nullptr;  // slice path: forward prefix at every chunk end
-    if (U == 1 && M > 0 && sl.fn) {
+    if (prep) {
+        Real* cb = nullptr;
+        e = alloc(reinterpret_cast<void**>(&ends), sizeof(Real) * B * U * D);
+        if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&cb), sizeof(Real) * B * U * D);
+        if (e == cudaSuccess) e = prep->vjp_prep_launch(X, B, L, prepU, (int)CL, U, cot, ends, cb, grad, s);
+        if (e != cudaSuccess) {
+            release();
+            return cuda_fail(e, "vjp fold-and-passes launch");
+        }
+        cbars = cb;
+        launches += 1;
+    } else if (U == 1 && M > 0 && sl.fn) {
         e = alloc(reinterpret_cast<void**>(&ends), sizeof(Real) * B * D);
         if (e != cudaSuccess) {
             release();
@@ -1352,7 +1416,7 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
         }
         launches += cst.launches;
     }
-    if (U > 1) {
+    if (U > 1 && !prep) {
         Real *Xseg = nullptr, *C = nullptr, *cb = nullptr;
         e = alloc(reinterpret_cast<void**>(&Xseg), sizeof(Real) * B * U * (CL + 1) * d);
         if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&C), sizeof(Real) * B * U * D);

@@ -15,6 +15,7 @@
 #include "path_kernel.cuh"
 #include "stream_kernel.cuh"
 #include "variants.h"
+#include "vjp_prep.cuh"
 
 namespace sigk {
 
@@ -269,6 +270,36 @@ struct PairVariant {
         return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, cl ? ckernel : kernel, threads(U), sm);
     }
 
+    // reverse mode's producer (vjp_prep.cuh), shapes with a slice walk only
+    static constexpr bool HAS_VJP = vjp_slice_q(DIM, DEPTH) > 0;
+    static std::atomic<uint64_t> vsmem_done;
+    static size_t vjp_smem(int U, int CL, int64_t L) { return vjp_prep_smem<DIM, DEPTH, Q>(U, CL, raw_floats(L - 1)); }
+    template <bool E = HAS_VJP>
+    static cudaError_t vjp_launch(const void* X, int64_t B, int64_t L, int U, int CL, int R, const void* cot,
+                                  void* ends, void* cbars, void* grad, cudaStream_t s) {
+        if constexpr (E) {
+            constexpr auto k = pair_vjp_prep_kernel<DIM, DEPTH, Q, NT>;
+            PairGeom g{};
+            g.G = 1;
+            g.SL = L - 1;
+            g.U = U;
+            g.UP = U / 2;
+            g.CL = CL;
+            g.threads = threads(U);
+            g.raw_floats = raw_floats(L - 1);
+            if (U % 2 || g.threads > NT) return cudaErrorInvalidValue;
+            const size_t sm = vjp_smem(U, CL, L);
+            cudaError_t e = opt_in_smem(k, sm, vsmem_done);
+            if (e != cudaSuccess) return e;
+            k<<<(unsigned)B, g.threads, sm, s>>>(static_cast<const float*>(X), L, g, R, static_cast<const float*>(cot),
+                                                  static_cast<float*>(ends), static_cast<float*>(cbars),
+                                                  static_cast<float*>(grad));
+            return cudaGetLastError();
+        } else {
+            return cudaErrorNotSupported;
+        }
+    }
+
     // prefix stream: one CTA per path; the largest stage tile TS in {8, 4, 2, 1} that fits
     static constexpr auto skernel = pair_stream_kernel<DIM, DEPTH, Q, NT, MINB>;
     static std::atomic<uint64_t> ssmem_done;
@@ -324,6 +355,8 @@ template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::pcsmem_done{0};
 template <int DIM, int DEPTH, int Q>
 std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::ssmem_done{0};
+template <int DIM, int DEPTH, int Q>
+std::atomic<uint64_t> PairVariant<DIM, DEPTH, Q>::vsmem_done{0};
 
 // Smallest Q whose pair state (two chunks) fits ~80 registers, or -1.
 constexpr int pick_q_pair(int d, int N) {
@@ -353,6 +386,10 @@ Variant make_pair_variant() {
     }
     v.stream_launch = &V::stream_launch;
     v.stream_tile_steps = &V::stream_tile_steps;
+    if constexpr (V::HAS_VJP) {
+        v.vjp_prep_launch = &V::template vjp_launch<true>;
+        v.vjp_prep_smem = &V::vjp_smem;
+    }
     return v;
 }
 

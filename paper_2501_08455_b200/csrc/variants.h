@@ -75,6 +75,12 @@ struct Variant {
     cudaError_t (*pair_pos_occupancy)(int U, int CL, int64_t SL, int G, bool cluster, int* blocks_per_sm);
     // pair family: stage tile (steps) of the prefix-stream launch for (L, G, U); 0: does not fit
     int (*stream_tile_steps)(int64_t L, int G, int U);
+    // pair family, reverse mode (vjp_prep.cuh): one CTA per path folds its U chunks (CL steps
+    // each, R real) and runs both chunk passes in shared memory -> ends / cbars rows (B, R, D)
+    // and zeros at the shared chunk points of grad; null where the shape has no slice walk
+    cudaError_t (*vjp_prep_launch)(const void* X, int64_t B, int64_t L, int U, int CL, int R, const void* cot,
+                                   void* ends, void* cbars, void* grad, cudaStream_t s);
+    size_t (*vjp_prep_smem)(int U, int CL, int64_t L);  // bytes of one CTA
 };
 
 const Variant* find_variant(int d, int N, bool is_f64);  // first (smallest-Q) candidate

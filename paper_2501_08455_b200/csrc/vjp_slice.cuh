@@ -175,7 +175,7 @@ struct SliceRev {
 // kernels in scalar form. With -δ it undoes a step (exp(-δ) is the inverse of
 // exp(δ)), which is how the backward walk recovers the states it needs.
 template <typename Real, int d, int N, int Q>
-struct SliceFold {
+struct VjpSliceFold {
     using LY = SliceLayout<d, N, Q>;
     static constexpr int S = LY::S, NLOW = LY::NLOW, VS = LY::VS;
     __device__ __forceinline__ static Real& sc(Real (&v)[S], int k) { return k < Q ? v[k - 1] : v[NLOW]; }
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(128) vjp_slice_kernel(const Real* __restrict__
             for (int c = 0; c < d; ++c) ndl[c] = -dl[c];
 #pragma unroll
             for (int k = 1; k <= Q; ++k) ndp[k] = -dp[k];
-            SliceFold<Real, d, N, Q>::template levels<N>(an, ndl, ndp);
+            VjpSliceFold<Real, d, N, Q>::template levels<N>(an, ndl, ndp);
             if (s == 0) {  // S_0: the identity, exactly (a branch, not S selects per step)
 #pragma unroll
                 for (int i = 0; i < S; ++i) an[i] = Real(0);
@@ -687,6 +687,90 @@ struct ScanPasses {
     __host__ __device__ static constexpr size_t smem(int U) { return ((size_t)U * D + (size_t)2 * U * DL + D) * sizeof(Real); }
 };
 
+// The two passes on shared-memory rows (any block size): Cs [U][D] the chunk
+// signatures, Es / Ts
+// [U][DL], cs [D] the output cotangent. FWD: E, written to the ends rows eb;
+// BWD: T, then the cbar rows cb. Barriers inside: every thread of the block calls it.
+template <typename Real, int d, int N, bool FWD, bool BWD>
+__device__ __forceinline__ void scan_passes_smem(Real* __restrict__ Cs, Real* __restrict__ Es, Real* __restrict__ Ts,
+                                                 const Real* __restrict__ cs, int U, Real* __restrict__ eb,
+                                                 Real* __restrict__ cb, int tid, int nth) {
+    constexpr int D = level_off(d, N), DL = level_off(d, N - 1);
+    // one barrier per level: the thread owning entry I of level n (of E, or of T) walks the
+    // chunks with the running sum in a register; the increment's loads (lower levels, done
+    // at earlier levels) do not depend on the sum, so consecutive chunks overlap
+#pragma unroll
+    for (int n = 1; n <= N; ++n) {
+        const int sz = ipow(d, n), on = level_off(d, n - 1);
+        const int nE = FWD ? sz : 0, nT = (BWD && n < N) ? sz : 0;  // T_N is never needed
+        for (int w = tid; w < nE + nT; w += nth) {
+            if (w < nE) {  // E_n^(j) = E_n^(j-1) + C_n^(j) + Σ_a E_a^(j-1) ⊗ C_{n-a}^(j)
+                const int I = w;
+                Real run = Real(0);
+                const Real* c = Cs + on + I;
+                Real* e = Es + on + I;
+                Real* g = eb + on + I;
+#pragma unroll 4
+                for (int j = 0; j < U; ++j) {
+                    Real x = c[(size_t)j * D];
+                    if (j > 0) {
+#pragma unroll
+                        for (int a = 1; a < n; ++a) {
+                            const int tail = ipow(d, n - a);
+                            x = fma(Es[(size_t)(j - 1) * DL + level_off(d, a - 1) + I / tail],
+                                    Cs[(size_t)j * D + level_off(d, n - a - 1) + I % tail], x);
+                        }
+                    }
+                    run += x;
+                    if (n < N) e[(size_t)j * DL] = run;
+                    g[(size_t)j * D] = run;
+                }
+            } else {  // T_n^(j) = T_n^(j+1) + C_n^(j+1) + Σ_a C_a^(j+1) ⊗ T_{n-a}^(j+1)
+                const int I = w - nE;
+                Real run = Real(0);
+                Real* t = Ts + on + I;
+                t[(size_t)(U - 1) * DL] = Real(0);
+#pragma unroll 4
+                for (int j = U - 2; j >= 0; --j) {
+                    Real y = Cs[(size_t)(j + 1) * D + on + I];
+#pragma unroll
+                    for (int a = 1; a < n; ++a) {
+                        const int tail = ipow(d, n - a);
+                        y = fma(Cs[(size_t)(j + 1) * D + level_off(d, a - 1) + I / tail],
+                                Ts[(size_t)(j + 1) * DL + level_off(d, n - a - 1) + I % tail], y);
+                    }
+                    run += y;
+                    t[(size_t)j * DL] = run;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if constexpr (BWD) {
+        // cbar rows, level by level (compile-time index structure; four partial sums:
+        // the level-1 entries carry ~D terms)
+#pragma unroll
+        for (int m = 1; m <= N; ++m) {
+            const int sz = ipow(d, m), om = level_off(d, m - 1);
+            for (int w = tid; w < U * sz; w += nth) {
+                const int j = w / sz, I = w - (w / sz) * sz;
+                Real acc[4] = {cs[om + I], Real(0), Real(0), Real(0)};
+                if (j < U - 1) {
+                    const Real* tj = Ts + (size_t)j * DL;
+#pragma unroll
+                    for (int k = 1; k <= N - m; ++k) {
+                        const Real* cr = cs + level_off(d, m + k - 1) + I * ipow(d, k);
+                        const Real* tr = tj + level_off(d, k - 1);
+#pragma unroll 16
+                        for (int J = 0; J < ipow(d, k); ++J) acc[J & 3] = fma(cr[J], tr[J], acc[J & 3]);
+                    }
+                }
+                cb[(size_t)j * D + om + I] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            }
+        }
+    }
+}
+
 template <typename Real, int d, int N>
 __global__ void __launch_bounds__(ScanPasses<Real, d, N>::NT) vjp_scan_passes_kernel(
     const Real* __restrict__ C, const Real* __restrict__ cot, int U, int, Real* __restrict__ cbars,
@@ -704,7 +788,6 @@ __global__ void __launch_bounds__(ScanPasses<Real, d, N>::NT) vjp_scan_passes_ke
     const int64_t b = blockIdx.x >> 1;
     const int tid = threadIdx.x;
     const Real* Cb = C + b * U * D;
-    Real* eb = ends + b * U * D;
     pdl_trigger();
     pdl_wait();
     if (fwd) {
@@ -728,93 +811,8 @@ __global__ void __launch_bounds__(ScanPasses<Real, d, N>::NT) vjp_scan_passes_ke
     if (!fwd)
         for (int i = tid; i < D; i += SP::NT) cs[i] = __ldcg(cot + b * D + i);
     __syncthreads();
-#pragma unroll
-    for (int n = 1; n <= N; ++n) {
-        if (!fwd && n == N) break;  // T_N is never needed
-        const int sz = ipow(d, n), on = level_off(d, n - 1);
-        // phase 1: increments. E: x^(j) = C_n^(j) + Σ_a E_a^(j-1) ⊗ C_{n-a}^(j) -> level n of
-        // E row j (of C row j for level N); T: y^(j) = C_n^(j+1) + Σ_a C_a^(j+1) ⊗
-        // T_{n-a}^(j+1) -> level n of T row j (row U-1: 0)
-        for (int w = tid; w < U * sz; w += SP::NT) {
-            const int j = w / sz, I = w - (w / sz) * sz;
-            if (fwd) {
-                Real x = Cs[(size_t)j * D + on + I];
-                if (j > 0) {
-#pragma unroll
-                    for (int a = 1; a < n; ++a) {
-                        const int tail = ipow(d, n - a);
-                        x = fma(Es[(size_t)(j - 1) * DL + level_off(d, a - 1) + I / tail],
-                                Cs[(size_t)j * D + level_off(d, n - a - 1) + I % tail], x);
-                    }
-                }
-                if (n < N) Es[(size_t)j * DL + on + I] = x;
-                else Cs[(size_t)j * D + on + I] = x;  // in place: no other item reads C_N^(j)[I]
-            } else {
-                Real y = Real(0);
-                if (j < U - 1) {
-                    y = Cs[(size_t)(j + 1) * D + on + I];
-#pragma unroll
-                    for (int a = 1; a < n; ++a) {
-                        const int tail = ipow(d, n - a);
-                        y = fma(Cs[(size_t)(j + 1) * D + level_off(d, a - 1) + I / tail],
-                                Ts[(size_t)(j + 1) * DL + level_off(d, n - a - 1) + I % tail], y);
-                    }
-                }
-                Ts[(size_t)j * DL + on + I] = y;
-            }
-        }
-        __syncthreads();
-        // phase 2: running sums over the chunks (E forwards, T backwards); the ends rows
-        for (int I = tid; I < sz; I += SP::NT) {
-            Real run = Real(0);
-            if (fwd && n < N) {
-                Real* e = Es + on + I;
-                Real* g = eb + on + I;
-                for (int j = 0; j < U; ++j) {
-                    run += e[(size_t)j * DL];
-                    e[(size_t)j * DL] = run;
-                    g[(size_t)j * D] = run;
-                }
-            } else if (fwd) {  // level N: the increments sit in the C rows
-                const Real* e = Cs + on + I;
-                Real* g = eb + on + I;
-                for (int j = 0; j < U; ++j) {
-                    run += e[(size_t)j * D];
-                    g[(size_t)j * D] = run;
-                }
-            } else {
-                Real* t = Ts + on + I;
-                for (int j = U - 1; j >= 0; --j) {
-                    run += t[(size_t)j * DL];
-                    t[(size_t)j * DL] = run;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    if (fwd) return;
-    // cbar rows, level by level (compile-time index structure; four partial sums:
-    // the level-1 entries carry ~D terms)
-    Real* cb = cbars + b * U * D;
-#pragma unroll
-    for (int m = 1; m <= N; ++m) {
-        const int sz = ipow(d, m), om = level_off(d, m - 1);
-        for (int w = tid; w < U * sz; w += SP::NT) {
-            const int j = w / sz, I = w - (w / sz) * sz;
-            Real acc[4] = {cs[om + I], Real(0), Real(0), Real(0)};
-            if (j < U - 1) {
-                const Real* tj = Ts + (size_t)j * DL;
-#pragma unroll
-                for (int k = 1; k <= N - m; ++k) {
-                    const Real* cr = cs + level_off(d, m + k - 1) + I * ipow(d, k);
-                    const Real* tr = tj + level_off(d, k - 1);
-#pragma unroll 16
-                    for (int J = 0; J < ipow(d, k); ++J) acc[J & 3] = fma(cr[J], tr[J], acc[J & 3]);
-                }
-            }
-            cb[(size_t)j * D + om + I] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        }
-    }
+    if (fwd) scan_passes_smem<Real, d, N, true, false>(Cs, Es, Ts, cs, U, ends + b * U * D, nullptr, tid, SP::NT);
+    else scan_passes_smem<Real, d, N, false, true>(Cs, Es, Ts, cs, U, nullptr, cbars + b * U * D, tid, SP::NT);
 }
 
 }  // namespace sigk

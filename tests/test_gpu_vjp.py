@@ -140,3 +140,20 @@ def test_signature_autograd_gradcheck_and_training_step(sk):
         ref = O.ref_vjp(X32.detach().double().cpu().numpy(), 4, cot)
         got = X32.grad.double().cpu().numpy()
         assert np.abs(got - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("B,L,d,N", [(4, 1000, 5, 4), (3, 1200, 3, 4), (2, 800, 2, 5), (5, 900, 4, 3)])
+def test_vjp_f32_fold_and_passes_in_one_launch(sk, B, L, d, N):
+    # fp32, one wave of paths long enough: one launch folds every path's chunks and runs
+    # both chunk passes in shared memory (vjp_prep.cuh), then the walk -- 2 launches
+    X = walk(B, L, d, seed=L + d).astype(np.float32)
+    cot = np.random.default_rng(d).standard_normal((B, sk.sig_dim(d, N))).astype(np.float32)
+    st = sk.KernelStats()
+    got = sk.signature_vjp(X, N, cot, stats=st)
+    assert st.launches == 2 and st.chunks >= 2, (st.launches, st.chunks)
+    ref = O.ref_vjp(X.astype(np.float64), N, cot.astype(np.float64))
+    assert rel(got, ref) <= 1e-4, rel(got, ref)
+    # the separate chunk-signature and pass launches at the same chunking agree
+    sep = sk.signature_vjp(X, N, cot, chunks=st.chunks, stats=st)
+    assert st.launches >= 3
+    assert rel(got, sep) <= 2e-5, rel(got, sep)

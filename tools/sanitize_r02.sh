@@ -1,7 +1,7 @@
 #!/bin/bash
 # compute-sanitizer over the round-2 device paths: the parallel (per-degree scan)
 # formulation and its reverse mode, the chunked reverse mode (in-place chunk
-# signatures, by-degree chunk passes), the cluster (DSMEM) segment combine, the position-table fold with its
+# signatures, by-degree chunk passes, the one-launch fold-and-passes), the cluster (DSMEM) segment combine, the position-table fold with its
 # producer warp (mbarrier pipeline), and the scratch-lifetime graph test.
 S=/usr/local/cuda/bin/compute-sanitizer
 cat > /tmp/san_r02.py <<'PY'
@@ -28,6 +28,14 @@ gs = sk.signature_vjp(X[:3].astype(np.float64), 3, cot, kernel=sk.KernelKind.Seq
 assert np.abs(gp - gs).max() <= 1e-10 * np.abs(gs).max()
 g32 = sk.signature_vjp(X[:3], 3, cot.astype(np.float32), chunks=6)
 assert np.abs(g32 - gs).max() <= 1e-4 * np.abs(gs).max()
+# fp32 fold-and-passes in one launch (vjp_prep.cuh): one wave of paths of >= 750 steps
+X2 = np.cumsum(rng.standard_normal((3, 801, 5)) * 0.03, axis=1).astype(np.float32)
+c2 = rng.standard_normal((3, 780)).astype(np.float32)
+st = sk.KernelStats()
+gp2 = sk.signature_vjp(X2, 4, c2, stats=st)
+assert st.launches == 2
+gs2 = sk.signature_vjp(X2.astype(np.float64), 4, c2.astype(np.float64))
+assert np.abs(gp2 - gs2).max() <= 1e-4 * np.abs(gs2).max()
 print("sanitized paths ok")
 PY
 for tool in memcheck racecheck synccheck; do
