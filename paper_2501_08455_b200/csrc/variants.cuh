@@ -278,7 +278,9 @@ struct PairVariant {
     static cudaError_t vjp_launch(const void* X, int64_t B, int64_t L, int U, int CL, int R, const void* cot,
                                   void* ends, void* cbars, void* grad, cudaStream_t s) {
         if constexpr (E) {
-            constexpr auto k = pair_vjp_prep_kernel<DIM, DEPTH, Q, NT>;
+            // 512 threads: the fold uses U/2 * P of them, the chunk passes all (<= 128 registers)
+            constexpr int NTV = 512;
+            constexpr auto k = pair_vjp_prep_kernel<DIM, DEPTH, Q, NTV>;
             PairGeom g{};
             g.G = 1;
             g.SL = L - 1;
@@ -291,7 +293,7 @@ struct PairVariant {
             const size_t sm = vjp_smem(U, CL, L);
             cudaError_t e = opt_in_smem(k, sm, vsmem_done);
             if (e != cudaSuccess) return e;
-            k<<<(unsigned)B, g.threads, sm, s>>>(static_cast<const float*>(X), L, g, R, static_cast<const float*>(cot),
+            k<<<(unsigned)B, NTV, sm, s>>>(static_cast<const float*>(X), L, g, R, static_cast<const float*>(cot),
                                                   static_cast<float*>(ends), static_cast<float*>(cbars),
                                                   static_cast<float*>(grad));
             return cudaGetLastError();
