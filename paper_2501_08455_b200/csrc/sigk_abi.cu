@@ -1342,13 +1342,12 @@ static int vjp_device(const Real* X, int64_t B, int64_t L, int d, int N, const R
     // fp32 shapes with a pair variant and a slice walk, paths short enough to fold in one
     // CTA: one launch folds every path's U chunks and runs both chunk passes in shared
     // memory (vjp_prep.cuh), replacing the chunk-signature launch, its rows and the pass
-    // launch. The walk's time does not depend on the chunk count (C2: 55.6 / 53.0 /
-    // 54.6 us at U = 9 / 18 / 36), so U is the CTA's widest chunking.
+    // launch; U is the CTA chunking (<= 2 * units_max) the walk's wave model prefers.
     const Variant* prep = nullptr;
     int prepU = 0;
     int64_t prepCL = 0;
     if constexpr (sizeof(Real) == 4) {
-        // one fold-and-passes CTA per path and SM (~160 registers x 256 threads): only
+        // one fold-and-passes CTA per path and SM (512 threads x 128 registers): only
         // batches that fit one wave (B = 1024, L = 200 measured 263 vs 80 us otherwise),
         // and paths long enough that the launches it saves outweigh its serial passes
         // (measured: 72 vs 76 us at 128 x 1000, 69 vs 74 at 32 x 2000; 29 vs 25 at
