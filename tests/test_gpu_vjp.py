@@ -157,3 +157,28 @@ def test_vjp_f32_fold_and_passes_in_one_launch(sk, B, L, d, N):
     sep = sk.signature_vjp(X, N, cot, chunks=st.chunks, stats=st)
     assert st.launches >= 3
     assert rel(got, sep) <= 2e-5, rel(got, sep)
+
+
+@pytest.mark.parametrize("L", [1000, 300])
+def test_vjp_graph_capture_replay(sk, L):
+    # reverse mode captured into a CUDA graph (the fold-and-passes launch at L = 1000, the
+    # three-launch form at L = 300) replays to the eager result, also after the stream's
+    # scratch grew in between
+    torch = pytest.importorskip("torch")
+    s = torch.cuda.Stream()
+    X = torch.from_numpy(walk(8, L, 5, seed=L).astype(np.float32)).cuda()
+    cot = torch.from_numpy(np.random.default_rng(L).standard_normal((8, 780)).astype(np.float32)).cuda()
+    with torch.cuda.stream(s):
+        eager = sk.signature_vjp(X, 4, cot).clone()
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        out = sk.signature_vjp(X, 4, cot)
+    big = torch.from_numpy(walk(64, L, 5, seed=L + 1).astype(np.float32)).cuda()
+    bcot = torch.randn(64, 780, device="cuda")
+    with torch.cuda.stream(s):
+        sk.signature_vjp(big, 4, bcot)  # may grow this stream's scratch
+        out.zero_()
+        g.replay()
+    s.synchronize()
+    assert torch.equal(out, eager)
