@@ -182,3 +182,17 @@ def test_vjp_graph_capture_replay(sk, L):
         g.replay()
     s.synchronize()
     assert torch.equal(out, eager)
+
+
+def test_vjp_prep_wave_boundary(sk):
+    # B = SMs: one fold-and-passes wave; B = SMs + 1: the three-launch form; same gradients
+    torch = pytest.importorskip("torch")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    X = walk(sms + 1, 800, 3, seed=77).astype(np.float32)
+    cot = np.random.default_rng(78).standard_normal((sms + 1, sk.sig_dim(3, 4))).astype(np.float32)
+    st = sk.KernelStats()
+    a = sk.signature_vjp(X[:sms], 4, cot[:sms], stats=st)
+    assert st.launches == 2
+    b = sk.signature_vjp(X, 4, cot, stats=st)
+    assert st.launches >= 3
+    assert rel(a, b[:sms]) <= 2e-5
