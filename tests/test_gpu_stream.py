@@ -118,3 +118,16 @@ def test_stream_segments(sk, G):
     got = sk.signature_stream(X, 4, stats=st, segments=G)
     assert st.segments == G, st
     assert max(errs(got, oracle_stream(X, 4), 5, 4)) <= F32_TOL
+
+
+@pytest.mark.parametrize("B,L,d,N", [(16, 1000, 5, 4), (8, 500, 10, 3), (8, 300, 3, 6)])
+def test_stream_f64_full_length(sk, B, L, d, N):
+    # fp64 prefix rows at full sequence length (the chunk-parallel generic stream since
+    # round 2: chunk signatures, prefix products, per-chunk walks) <= 1e-12 against the oracle
+    rng = np.random.default_rng(B * L + d)
+    X = np.zeros((B, L, d))
+    X[:, 1:] = np.cumsum(rng.standard_normal((B, L - 1, d)) / np.sqrt(L - 1), axis=1)
+    got = sk.signature_stream(X, N)
+    _, ref = O.signature(X, N, threads=os.cpu_count() or 1, stream=True)
+    assert got.shape == ref.shape
+    assert max(errs(got, ref, d, N)) <= F64_TOL
