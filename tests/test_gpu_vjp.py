@@ -196,3 +196,13 @@ def test_vjp_prep_wave_boundary(sk):
     b = sk.signature_vjp(X, 4, cot, stats=st)
     assert st.launches >= 3
     assert rel(a, b[:sms]) <= 2e-5
+
+
+@pytest.mark.parametrize("B,L,d,N", [(16, 1000, 5, 4), (8, 500, 10, 3), (4, 10000, 5, 4)])
+def test_vjp_f64_full_length(sk, B, L, d, N):
+    # fp64 reverse mode at the BASELINE path lengths (C2 and C3 shapes on a row subset,
+    # C4's d = 10 at depth 3: the element-parallel adjoint) against the reference's adjoint
+    X = walk(B, L, d, seed=L + d)
+    cot = np.random.default_rng(L + 1).standard_normal((B, sk.sig_dim(d, N)))
+    got = sk.signature_vjp(X, N, cot)
+    assert rel(got, O.ref_vjp(X, N, cot)) <= 1e-10
