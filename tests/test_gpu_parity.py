@@ -293,3 +293,18 @@ def test_generic_chunk_parallel_long_paths(sk, B, L, d, N):
     rows = sk.signature_stream(X, N, family=sk.FAMILY_GENERIC)
     _, ref_rows = O.signature(X[:2], N, stream=True)
     assert np.max(np.abs(rows[:2] - ref_rows)) <= 1e-12 * np.max(np.abs(ref_rows))
+
+
+@pytest.mark.parametrize("B,L,d,N", [(2, 200001, 3, 4), (1, 100001, 5, 4), (3, 50001, 2, 6)])
+def test_very_long_paths(sk, B, L, d, N):
+    # paths far longer than any BASELINE config: many segments per path (in-launch
+    # segment combine) in fp32, fp64 against the oracle at 1e-12
+    X = brownian(B, L, d, seed=L % 1000)
+    st = sk.KernelStats()
+    X32 = X.astype(np.float32)
+    ref32 = O.signature(X32.astype(np.float64), N, threads=THREADS)
+    own = max(level_errors(O.signature(X32, N), ref32, d, N))  # the reference's own float error
+    got = sk.signature(X32, N, stats=st)
+    assert max(level_errors(got, ref32, d, N)) <= max(F32_TOL, 4 * own)
+    assert st.path_steps == L - 1
+    assert max(level_errors(sk.signature(X, N), O.signature(X, N, threads=THREADS), d, N)) <= 1e-12
