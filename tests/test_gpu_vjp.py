@@ -206,3 +206,17 @@ def test_vjp_f64_full_length(sk, B, L, d, N):
     cot = np.random.default_rng(L + 1).standard_normal((B, sk.sig_dim(d, N)))
     got = sk.signature_vjp(X, N, cot)
     assert rel(got, O.ref_vjp(X, N, cot)) <= 1e-10
+
+
+def test_vjp_very_long_paths(sk):
+    # 100K steps per path, two paths: hundreds of chunks per path (the chunk passes
+    # stream their rows instead of staging them), fp64 and fp32 against the reference
+    X = walk(2, 100001, 3, seed=91)
+    cot = np.random.default_rng(92).standard_normal((2, sk.sig_dim(3, 4)))
+    st = sk.KernelStats()
+    ref = O.ref_vjp(X, 4, cot)
+    assert rel(sk.signature_vjp(X, 4, cot, stats=st), ref) <= 1e-10
+    assert st.chunks > 100
+    g32 = sk.signature_vjp(X.astype(np.float32), 4, cot.astype(np.float32))
+    ref32 = O.ref_vjp(X.astype(np.float32).astype(np.float64), 4, cot.astype(np.float32).astype(np.float64))
+    assert rel(g32, ref32) <= 1e-4, rel(g32, ref32)
