@@ -131,3 +131,17 @@ def test_stream_f64_full_length(sk, B, L, d, N):
     _, ref = O.signature(X, N, threads=os.cpu_count() or 1, stream=True)
     assert got.shape == ref.shape
     assert max(errs(got, ref, d, N)) <= F64_TOL
+
+
+def test_stream_very_long_paths(sk):
+    # 100K-step prefix streams (segments chained by in-launch look-back), fp64 and fp32
+    rng = np.random.default_rng(101)
+    X = np.zeros((2, 100001, 3))
+    X[:, 1:] = np.cumsum(rng.standard_normal((2, 100000, 3)) / np.sqrt(100000), axis=1)
+    _, ref = O.signature(X, 4, threads=os.cpu_count() or 1, stream=True)
+    assert max(errs(sk.signature_stream(X, 4), ref, 3, 4)) <= F64_TOL
+    X32 = X.astype(np.float32)
+    _, ref32 = O.signature(X32.astype(np.float64), 4, threads=os.cpu_count() or 1, stream=True)
+    _, own = O.signature(X32, 4, stream=True)  # the reference's own float error
+    bar = max(F32_TOL, 4 * max(errs(own, ref32, 3, 4)))
+    assert max(errs(sk.signature_stream(X32, 4), ref32, 3, 4)) <= bar
