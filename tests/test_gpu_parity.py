@@ -308,3 +308,18 @@ def test_very_long_paths(sk, B, L, d, N):
     assert max(level_errors(got, ref32, d, N)) <= max(F32_TOL, 4 * own)
     assert st.path_steps == L - 1
     assert max(level_errors(sk.signature(X, N), O.signature(X, N, threads=THREADS), d, N)) <= 1e-12
+
+
+@pytest.mark.parametrize("B,L,d,N", [(500000, 3, 4, 4), (200000, 2, 5, 3), (100000, 17, 2, 5)])
+def test_very_large_batches_of_short_paths(sk, B, L, d, N):
+    # hundreds of thousands of short paths in one call (grids far past one wave); rows
+    # checked on a random sample against the oracle
+    X = brownian(B, L, d, seed=B % 997)
+    X32 = X.astype(np.float32)
+    got32 = sk.signature(X32, N)
+    got64 = sk.signature(X, N)
+    rows = np.random.default_rng(B).choice(B, 512, replace=False)
+    ref = O.signature(X[rows], N)
+    ref32 = O.signature(X32[rows].astype(np.float64), N)
+    assert max(level_errors(got64[rows], ref, d, N)) <= 1e-12
+    assert max(level_errors(got32[rows], ref32, d, N)) <= F32_TOL
