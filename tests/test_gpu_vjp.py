@@ -220,3 +220,12 @@ def test_vjp_very_long_paths(sk):
     g32 = sk.signature_vjp(X.astype(np.float32), 4, cot.astype(np.float32))
     ref32 = O.ref_vjp(X.astype(np.float32).astype(np.float64), 4, cot.astype(np.float32).astype(np.float64))
     assert rel(g32, ref32) <= 1e-4, rel(g32, ref32)
+
+
+def test_vjp_very_large_batch(sk):
+    # 200K short paths in one reverse-mode call, rows sampled against the reference
+    X = walk(200000, 12, 3, seed=93)
+    cot = np.random.default_rng(94).standard_normal((200000, sk.sig_dim(3, 4)))
+    g = sk.signature_vjp(X, 4, cot)
+    rows = np.random.default_rng(95).choice(200000, 256, replace=False)
+    assert rel(g[rows], O.ref_vjp(X[rows], 4, cot[rows])) <= 1e-10
