@@ -142,7 +142,8 @@ def test_signature_autograd_gradcheck_and_training_step(sk):
         assert np.abs(got - ref).max() <= 1e-4 * np.abs(ref).max()
 
 
-@pytest.mark.parametrize("B,L,d,N", [(4, 1000, 5, 4), (3, 1200, 3, 4), (2, 800, 2, 5), (5, 900, 4, 3)])
+@pytest.mark.parametrize("B,L,d,N", [(4, 1000, 5, 4), (3, 1200, 3, 4), (2, 800, 2, 5), (5, 900, 4, 3), (4, 1000, 1, 5),
+                                     (2, 900, 6, 3), (3, 1500, 8, 2)])
 def test_vjp_f32_fold_and_passes_in_one_launch(sk, B, L, d, N):
     # fp32, one wave of paths long enough: one launch folds every path's chunks and runs
     # both chunk passes in shared memory (vjp_prep.cuh), then the walk -- 2 launches
